@@ -1,0 +1,365 @@
+#!/usr/bin/env python
+"""Throughput benchmark: depth maps/s of fill_in_fast on B200 (BASELINE config 1).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1)
+
+One step = one pass of the pipeline over this rank's batch of
+``--frames`` (default 1024) synthetic 1216x352 frames (config 1:
+fill_in_fast(max_depth=100, diamond5, extrapolate=True, blur_type='gaussian'),
+density U(4 %, 6 %)).  Frames are independent, so ranks take disjoint frame
+ranges with no collective on the data path ("scaling": "weak").  ``value`` is
+whole-job frames/s with inputs resident in HBM; ``e2e`` is the same metric
+through the host-buffer API (pinned host in -> GPU -> pinned host out, copies
+inside the timed region).  ``--impl reference`` times the reference CPU path
+(oracle/_ref compiled reference kernels under the oracle orchestration, all
+host cores) on the same config.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "depth maps/sec at 1216×352 (1/2/4/8 B200) and % of HBM roofline"
+UNIT = "frames/s"
+CONFIG_ID = 1
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--frames", type=int, default=1024, help="frames per rank per step")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU-baseline sample length")
+    p.add_argument("--force-staged", action="store_true", help="time the staged (unfused) path instead")
+    return p.parse_args()
+
+
+def peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:  # noqa: BLE001
+        return {}
+
+
+def hbm_peak():
+    pk = peaks()
+    if "hbm_gbs" in pk:
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def gen_frames(start, count, procs=None):
+    """Config-1 frames [start, start+count), generated on the host in parallel."""
+    from multiprocessing import get_context
+
+    from paper_1802_00036_b200 import synth
+
+    procs = procs or max(1, min(16, (os.cpu_count() or 1)))
+    spec = synth.CONFIG_SPECS[CONFIG_ID]
+    out = np.empty((count, spec.height, spec.width), dtype=np.float32)
+    step = max(1, (count + procs - 1) // procs)
+    parts = [(start + a, min(count - a, step)) for a in range(0, count, step)]
+    with get_context("fork").Pool(len(parts)) as pool:
+        res = pool.starmap(synth.make_batch, [(CONFIG_ID, s, n) for s, n in parts])
+    a = 0
+    for r in res:
+        out[a: a + r.shape[0]] = r
+        a += r.shape[0]
+    return out
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:  # noqa: BLE001
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:  # noqa: BLE001
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline_leg(frames, seconds):
+    """Reference CPU path on a bounded sample of the same workload, all host cores."""
+    from oracle import cpu_baseline as C
+    from oracle import depthfill_oracle as O
+
+    cfg = O.OracleConfig(blur_mode=O.BlurMode.GAUSSIAN, fill_mode=O.FillMode.FULL)
+    kind = C.available_kind()
+    one = C.single_frame_seconds(frames[0], cfg, kind)
+    procs = os.cpu_count() or 1
+    n = int(max(procs, min(4096, seconds * procs / max(one, 1e-4))))
+    sample = frames[: min(len(frames), 256)]
+    r = C.time_cpu(sample, cfg, n, procs, kind)
+    return {"value": round(r["value"], 3), "unit": UNIT, "cores": r["cores"], "kind": kind,
+            "sample": f"{n} config-1 frames (cycling over {len(sample)} distinct) on {procs} worker processes, "
+                      f"1 thread each; {r['seconds']:.1f} s; single-thread {one * 1e3:.1f} ms/frame",
+            "cpu_model": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def config_block(B, args):
+    return {"workload": f"BASELINE config 1: fill_in_fast(max_depth=100, 5x5 diamond, extrapolate=True, "
+                        f"blur_type='gaussian') on {B} synthetic 1216x352 frames per GPU",
+            "frames_per_gpu": B, "width": 1216, "height": 352, "density": "U(4%,6%)",
+            "l2": "no flush needed: each step streams 2 x %.2f GB (> 126 MB L2)" % (B * 1216 * 352 * 4 / 1e9),
+            "parallelism": f"frame-sharded dp{args.gpus}, no collective",
+            "path": "staged" if args.force_staged else "fused"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import cpu_baseline as C
+    from oracle import depthfill_oracle as O
+
+    frames = gen_frames(0, 64)
+    cfg = O.OracleConfig(blur_mode=O.BlurMode.GAUSSIAN, fill_mode=O.FillMode.FULL)
+    procs = os.cpu_count() or 1
+    pool, procs, kind = C.make_pool(frames, cfg, procs)
+    per_step = 2 * procs
+    try:
+        for _ in range(args.warmup):
+            pool.map(C._work, range(per_step), chunksize=1)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            pool.map(C._work, range(per_step), chunksize=1)
+        dt = time.perf_counter() - t0
+    finally:
+        pool.close()
+        pool.join()
+    value = per_step * args.steps / dt
+    line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, SURVEY 8(d))",
+            "impl": "reference",
+            "config": {**config_block(args.frames, args), "reference_step": f"{per_step} frames per step"},
+            "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": procs, "kind": kind,
+                             "sample": f"{per_step} frames/step x {args.steps} steps over 64 distinct frames",
+                             "cpu_model": _cpu_model()},
+            "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1802_00036_b200 import _lib, ops
+    from paper_1802_00036_b200.completion import (BlurMode, FillMode, HostPipeline, PipelineConfig,
+                                                  raise_for_status, to_dfc_config)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    B = args.frames
+    host = gen_frames(rank * B, B)
+    x = torch.from_numpy(host).to(dev)
+    out = torch.empty_like(x)
+    status = torch.empty(B, dtype=torch.int32, device=dev)
+    iters = torch.empty(B, dtype=torch.int32, device=dev)
+    config = PipelineConfig(blur_mode=BlurMode.GAUSSIAN, fill_mode=FillMode.FULL, max_depth=100.0)
+    cfg = to_dfc_config(config, force_staged=args.force_staged)
+    cfg.flags |= _lib.F_NO_FINISH
+    L = _lib.load()
+    need = int(L.dfc_workspace_bytes(ctypes.byref(cfg), B, 352, 1216))
+    ws = torch.empty(need, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    P = ops._ptr  # noqa: SLF001
+
+    def step(ev0=None, ev1=None):
+        if ev0 is not None:
+            ev0.record(stream)
+        _lib.check(L.dfc_fill_batch(P(x), P(out), B, 352, 1216, ctypes.byref(cfg), P(status), P(iters), P(ws),
+                                    ws.numel(), sp))
+        if ev1 is not None:
+            ev1.record(stream)
+        _lib.check(L.dfc_fill_finish(P(x), P(out), B, 352, 1216, ctypes.byref(cfg), P(status), P(iters), P(ws),
+                                     ws.numel(), sp))
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    st = status.cpu().numpy()
+    raise_for_status(st, 100.0)
+    n_fallback = int(np.count_nonzero(st & _lib.ST_FALLBACK))
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = L.dfc_kernel_launches()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0e.record(stream)
+    for k in range(args.steps):
+        step(*kev[k])
+    t1e.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = int(L.dfc_kernel_launches() - launches0)
+    elapsed_ms = t0e.elapsed_time(t1e)
+    kern_ms = float(np.mean([a.elapsed_time(b) for a, b in kev]))
+    clk = clocks.stop()
+    t = torch.tensor([elapsed_ms, kern_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed_ms, kern_ms = float(t[0]), float(t[1])
+    ms_step = elapsed_ms / args.steps
+    value = world * B * args.steps / (elapsed_ms / 1e3)
+
+    # ---- e2e: host buffers through the public API -------------------------
+    e2e = None
+    if not args.no_e2e:
+        pipe = HostPipeline(config, chunk=64)
+        h_in = torch.from_numpy(host).pin_memory()
+        h_out = torch.empty_like(h_in).pin_memory()
+        for _ in range(2):
+            pipe.run(h_in, h_out)
+        e_steps = max(2, min(args.steps, 5))
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(e_steps):
+            pipe.run(h_in, h_out)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        td = torch.tensor([dt], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(td, op=dist.ReduceOp.MAX)
+        e2e = {"value": round(world * B * e_steps / float(td[0]), 3), "unit": UNIT,
+               "h2d_bytes_per_step": int(h_in.numel() * 4) * world, "d2h_bytes_per_step": int(h_out.numel() * 4) * world,
+               "path": "pinned host -> H2D -> dfc_fill_batch -> D2H, 64-frame chunks on 3 streams, wall clock"}
+        ok = bool(torch.equal(h_out, out.cpu()))
+        e2e["matches_device_path"] = ok
+
+    # ---- roofline of the dominant kernel ---------------------------------
+    pk, pk_src = hbm_peak()
+    alg_bytes = 8 * 1216 * 352 * B  # one f32 read + one f32 write per pixel
+    achieved = alg_bytes / (kern_ms / 1e3) / 1e9
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists():
+        try:
+            td = json.loads(tf.read_text())
+            key = "staged" if args.force_staged else "fused"
+            if key in td:
+                traffic = td[key]["dram_bytes_per_frame"] * B
+        except Exception:  # noqa: BLE001
+            traffic = None
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk, "unit": "GB/s",
+            "frac": round(achieved / pk, 4), "traffic": traffic, "peak_source": pk_src,
+            "algorithmic_bytes_per_launch": alg_bytes, "kernel_ms_per_launch": round(kern_ms, 4),
+            "kernel": "dfc_fill_batch (fused pipeline kernel + status memsets), CUDA events on its stream"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline_leg(host, args.cpu_seconds)
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "error": repr(e)}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": max(args.warmup, 3), "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, SURVEY 8(d))",
+                "config": config_block(B, args), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "clocks": clk, "gpu_launches": launches, "fallback_frames_per_step": n_fallback,
+                "gpu": torch.cuda.get_device_name(dev)}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,543 @@
+// extern "C" entry points of libdfc.so (include/dfc.h), argument checking,
+// and the staged (one op per launch) pipeline used when the fused kernel does
+// not cover a configuration and for frames that need more than one
+// large-fill iteration.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "dfc_common.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define DFC_CK(expr)                                                                          \
+  do {                                                                                        \
+    cudaError_t e_ = (expr);                                                                  \
+    if (e_ != cudaSuccess) return fail(DFC_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+bool odd3(int v) { return v >= 3 && (v % 2) == 1; }
+
+int check_shape(int64_t B, int32_t H, int32_t W) {
+  if (B < 0) return fail(DFC_E_INVALID, "batch size must be >= 0");
+  if (H < 1 || W < 1) return fail(DFC_E_INVALID, "depth map dimensions must be >= 1, got " +
+                                                      std::to_string(W) + "x" + std::to_string(H));
+  if ((int64_t)H * W > (int64_t)1 << 31)
+    return fail(DFC_E_INVALID, "depth map dimensions " + std::to_string(W) + "x" + std::to_string(H) +
+                                   " exceed supported size");
+  return DFC_OK;
+}
+
+// PipelineConfig.__post_init__ (pipeline.py:71-89)
+int check_config(const dfc_config& c) {
+  const struct {
+    const char* name;
+    int v;
+  } sizes[] = {{"dilation_size", c.dilation_size},     {"closure_size", c.closure_size},
+               {"small_fill_size", c.small_fill_size}, {"large_fill_size", c.large_fill_size},
+               {"median_size", c.median_size},         {"gaussian_size", c.gaussian_size},
+               {"bilateral_size", c.bilateral_size}};
+  for (auto& s : sizes)
+    if (!odd3(s.v))
+      return fail(DFC_E_INVALID, std::string(s.name) + " must be an odd integer >= 3, got " + std::to_string(s.v));
+  if (c.large_fill_max_iters < 1) return fail(DFC_E_INVALID, "large_fill_max_iters must be >= 1");
+  if (!(c.gaussian_sigma > 0)) return fail(DFC_E_INVALID, "gaussian_sigma must be positive");
+  if (!(c.bilateral_sigma_value > 0) || !(c.bilateral_sigma_space > 0))
+    return fail(DFC_E_INVALID, "bilateral sigmas must be positive");
+  if (c.dilation_shape < 0 || c.dilation_shape > 3) return fail(DFC_E_INVALID, "unknown kernel shape");
+  if (c.blur_mode < 0 || c.blur_mode > 5) return fail(DFC_E_INVALID, "unknown blur mode");
+  if (c.fill_mode < 0 || c.fill_mode > 1) return fail(DFC_E_INVALID, "unknown fill mode");
+  if (!std::isfinite(c.max_depth) || !(c.max_depth > 0.1f)) return fail(DFC_E_INVALID, "max_depth must be > 0.1");
+  if (c.gaussian_size > 63) return fail(DFC_E_UNSUPPORTED, "gaussian_size > 63 not supported");
+  if (c.custom_n < 0 || (c.custom_n > 0 && !c.custom_offsets)) return fail(DFC_E_INVALID, "bad custom kernel");
+  if (c.custom_n > 4096) return fail(DFC_E_UNSUPPORTED, "custom kernel with more than 4096 taps");
+  for (int t = 0; t < 2 * c.custom_n; ++t)
+    if (c.custom_offsets[t] < -127 || c.custom_offsets[t] > 127)
+      return fail(DFC_E_UNSUPPORTED, "custom kernel offset magnitude > 127");
+  if (c.multiscale) {
+    const int ks[3][2] = {{c.near_shape, c.near_size}, {c.med_shape, c.med_size}, {c.far_shape, c.far_size}};
+    for (auto& k : ks) {
+      if (k[0] < 0 || k[0] > 3) return fail(DFC_E_INVALID, "unknown kernel shape");
+      if (!odd3(k[1])) return fail(DFC_E_INVALID, "bin kernel size must be an odd integer >= 3");
+    }
+    if (!(c.bin_edge_near < c.bin_edge_far)) return fail(DFC_E_INVALID, "bin edges must be increasing");
+  }
+  return DFC_OK;
+}
+
+// pipeline._fit_to_frame (:241-254) -- also applied to the multiscale bin kernels
+dfc_config fit_to_frame(const dfc_config& c, int H, int W) {
+  dfc_config o = c;
+  const int limit = 2 * (H < W ? H : W) + 1;
+  const int fit = limit > 3 ? limit : 3;
+  int* fields[] = {&o.dilation_size, &o.closure_size, &o.small_fill_size, &o.large_fill_size,
+                   &o.near_size,     &o.med_size,     &o.far_size};
+  for (int* f : fields)
+    if (*f > limit) *f = fit;
+  return o;
+}
+
+// make_kernel + kernel_offsets (kernels.py:45-78): row-major (dy,dx) list
+std::vector<int32_t> kernel_offsets(int shape, int size, bool* is_full) {
+  std::vector<int32_t> o;
+  const int r = size / 2;
+  bool full = true;
+  for (int dy = -r; dy <= r; ++dy)
+    for (int dx = -r; dx <= r; ++dx) {
+      bool on;
+      switch (shape) {
+        case DFC_SHAPE_FULL: on = true; break;
+        case DFC_SHAPE_DIAMOND: on = std::abs(dx) + std::abs(dy) <= r; break;
+        case DFC_SHAPE_CROSS: on = dx == 0 || dy == 0; break;
+        default: on = 4 * (dx * dx + dy * dy) <= size * size; break;
+      }
+      if (on) {
+        o.push_back(dy);
+        o.push_back(dx);
+      } else {
+        full = false;
+      }
+    }
+  *is_full = full;
+  return o;
+}
+
+// ---- staged pipeline -------------------------------------------------------
+
+struct StagedBufs {
+  float *a, *b, *c, *d, *e;  // e follows d: (d,e) doubles as a float64 scratch
+  int64_t *n_valid, *counts;
+  unsigned long long* total;
+};
+
+int64_t staged_chunk(int64_t B, int H, int W) {
+  const int64_t per = (int64_t)H * W * 4;
+  int64_t c = ((int64_t)64 << 20) / per;
+  if (c < 1) c = 1;
+  return c < B ? c : B;
+}
+
+size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
+
+size_t staged_bytes(int64_t chunk, int H, int W) {
+  if (chunk <= 0) return 0;
+  const size_t f = align256((size_t)chunk * H * W * 4);
+  return 5 * f + align256(chunk * 8) * 2 + 256;
+}
+
+StagedBufs carve_staged(void* ws, int64_t chunk, int H, int W) {
+  char* p = static_cast<char*>(ws);
+  const size_t f = align256((size_t)chunk * H * W * 4);
+  StagedBufs s;
+  s.a = (float*)p;
+  s.b = (float*)(p + f);
+  s.c = (float*)(p + 2 * f);
+  s.d = (float*)(p + 3 * f);
+  s.e = (float*)(p + 4 * f);
+  s.n_valid = (int64_t*)(p + 5 * f);
+  s.counts = (int64_t*)(p + 5 * f + align256(chunk * 8));
+  s.total = (unsigned long long*)(p + 5 * f + 2 * align256(chunk * 8));
+  return s;
+}
+
+cudaError_t dilate_any(const float* in, float* out, float* tmp, int64_t B, int H, int W, int shape, int size,
+                       bool is_min, cudaStream_t s) {
+  bool full;
+  auto offs = kernel_offsets(shape, size, &full);
+  if (full) {
+    cudaError_t e = dfc::launch_line_minmax(in, tmp, B, H, W, size / 2, is_min, 1, s);
+    if (e != cudaSuccess) return e;
+    return dfc::launch_line_minmax(tmp, out, B, H, W, size / 2, is_min, 0, s);
+  }
+  return dfc::launch_offsets_minmax(in, out, B, H, W, offs.data(), (int)offs.size() / 2, is_min, s);
+}
+
+int gaussian_weights(int size, double sigma, double* w) {
+  // morphology.gaussian_weights (:128-133)
+  const int r = size / 2;
+  double sum = 0.0;
+  for (int i = -r; i <= r; ++i) {
+    w[i + r] = std::exp(-(double)(i * i) / (2.0 * sigma * sigma));
+  }
+  for (int i = 0; i < size; ++i) sum += w[i];  // np.sum pairwise == sequential for <= 8 terms
+  for (int i = 0; i < size; ++i) w[i] /= sum;
+  return size;
+}
+
+int run_staged(const float* in, float* out, int64_t B, int H, int W, const dfc_config& c, uint32_t* status,
+               int32_t* iters, void* ws, size_t ws_bytes, cudaStream_t s) {
+  const int64_t chunk = staged_chunk(B, H, W);
+  if (!ws || ws_bytes < staged_bytes(chunk, H, W)) return fail(DFC_E_WORKSPACE, "workspace too small (staged)");
+  const int64_t HW = (int64_t)H * W;
+  const bool full = c.fill_mode == DFC_FILL_FULL;
+  const bool exact = (c.flags & DFC_F_EXACT_BLUR) != 0;
+  double gw[64];
+  gaussian_weights(c.gaussian_size, c.gaussian_sigma, gw);
+  for (int64_t f0 = 0; f0 < B; f0 += chunk) {
+    const int64_t C = B - f0 < chunk ? B - f0 : chunk;
+    StagedBufs q = carve_staged(ws, chunk, H, W);
+    const float* x = in + f0 * HW;
+    float* y = out + f0 * HW;
+    uint32_t* st = status + f0;
+    int32_t* it = iters ? iters + f0 : nullptr;
+    const int64_t n = C * HW;
+    DFC_CK(cudaMemsetAsync(q.n_valid, 0, C * 8, s));
+    DFC_CK(dfc::launch_validate(x, HW, C, st, q.n_valid, s));
+    DFC_CK(dfc::launch_finalize_status(q.n_valid, st, C, s));
+    // 1. invert
+    DFC_CK(dfc::launch_invert(x, q.a, HW, C, c.max_depth, st, s));
+    // 2. shaped dilation (or depth-binned multiscale dilation)
+    if (!c.multiscale && c.custom_n > 0) {
+      DFC_CK(dfc::launch_offsets_minmax(q.a, q.b, C, H, W, c.custom_offsets, c.custom_n, false, s));
+    } else if (!c.multiscale) {
+      DFC_CK(dilate_any(q.a, q.b, q.d, C, H, W, c.dilation_shape, c.dilation_size, false, s));
+    } else {
+      const float inf = INFINITY;
+      const float lo[3] = {-inf, c.bin_edge_near, c.bin_edge_far};
+      const float hi[3] = {c.bin_edge_near, c.bin_edge_far, inf};
+      const int shp[3] = {c.near_shape, c.med_shape, c.far_shape};
+      const int siz[3] = {c.near_size, c.med_size, c.far_size};
+      for (int k = 0; k < 3; ++k) {
+        DFC_CK(dfc::launch_bin_select(x, q.a, q.c, n, lo[k], hi[k], s));
+        DFC_CK(dilate_any(q.c, k == 0 ? q.b : q.e, q.d, C, H, W, shp[k], siz[k], false, s));
+        if (k > 0) DFC_CK(dfc::launch_max2(q.b, q.e, q.b, n, s));
+      }
+    }
+    // 3. close (FULL closure_size)
+    DFC_CK(dilate_any(q.b, q.c, q.d, C, H, W, DFC_SHAPE_FULL, c.closure_size, false, s));
+    DFC_CK(dilate_any(q.c, q.b, q.d, C, H, W, DFC_SHAPE_FULL, c.closure_size, true, s));
+    // 4. small masked fill
+    DFC_CK(dilate_any(q.b, q.c, q.d, C, H, W, DFC_SHAPE_FULL, c.small_fill_size, false, s));
+    DFC_CK(dfc::launch_masked_fill(q.b, q.c, q.a, n, s));
+    float* cur = q.a;
+    float* spare = q.b;
+    if (full) {
+      // 5. extend to top
+      DFC_CK(dfc::launch_extend_to_top(q.a, q.b, C, H, W, s));
+      cur = q.b;
+      spare = q.a;
+      // 6. large fill, iterated per frame while empties remain
+      for (int k = 0; k < c.large_fill_max_iters; ++k) {
+        DFC_CK(cudaMemsetAsync(q.counts, 0, C * 8, s));
+        DFC_CK(cudaMemsetAsync(q.total, 0, 8, s));
+        DFC_CK(dfc::launch_count_empty(cur, HW, C, q.counts, s));
+        DFC_CK(dfc::launch_iter_update(q.counts, it, C, q.total, s));
+        unsigned long long total = 0;
+        DFC_CK(cudaMemcpyAsync(&total, q.total, 8, cudaMemcpyDeviceToHost, s));
+        DFC_CK(cudaStreamSynchronize(s));
+        if (total == 0) break;
+        DFC_CK(dilate_any(cur, q.c, q.d, C, H, W, DFC_SHAPE_FULL, c.large_fill_size, false, s));
+        DFC_CK(dfc::launch_masked_fill(cur, q.c, cur, n, s));
+      }
+    }
+    // 7. blur stage (pipeline._blur_stage :206-238)
+    const int bm = c.blur_mode;
+    const bool partial = !full;
+    if (bm == DFC_BLUR_MEDIAN || bm == DFC_BLUR_MEDIAN_BILATERAL || bm == DFC_BLUR_MEDIAN_GAUSSIAN) {
+      DFC_CK(dfc::launch_median(cur, q.c, C, H, W, c.median_size, s));
+      if (partial) DFC_CK(dfc::launch_reimpose(q.c, cur, q.c, n, s));
+      std::swap(cur, q.c);
+      if (cur == q.c) std::swap(q.c, spare);
+    }
+    if (bm == DFC_BLUR_GAUSSIAN || bm == DFC_BLUR_MEDIAN_GAUSSIAN) {
+      DFC_CK(dfc::launch_gauss_line(cur, q.d, C, H, W, gw, c.gaussian_size, 1, exact, false, exact, s));
+      DFC_CK(dfc::launch_gauss_line((const float*)q.d, spare, C, H, W, gw, c.gaussian_size, 0, exact, exact,
+                                    false, s));
+      if (partial) DFC_CK(dfc::launch_reimpose(spare, cur, spare, n, s));
+      std::swap(cur, spare);
+    }
+    if (bm == DFC_BLUR_BILATERAL || bm == DFC_BLUR_MEDIAN_BILATERAL) {
+      DFC_CK(dfc::launch_bilateral(cur, spare, C, H, W, c.bilateral_size, c.bilateral_sigma_value,
+                                   c.bilateral_sigma_space, exact, s));
+      if (partial) DFC_CK(dfc::launch_reimpose(spare, cur, spare, n, s));
+      std::swap(cur, spare);
+    }
+    // 8. invert back
+    DFC_CK(dfc::launch_invert(cur, y, HW, C, c.max_depth, nullptr, s));
+  }
+  return DFC_OK;
+}
+
+// workspace layout: [fused region][staged region]
+struct WsLayout {
+  size_t fused, staged, total;
+  int64_t chunk;
+  bool use_fused;
+};
+
+WsLayout ws_layout(const dfc_config& c, int64_t B, int H, int W) {
+  WsLayout L;
+  L.use_fused = !(c.flags & DFC_F_FORCE_STAGED) && dfc::fused_supported(c, H, W);
+  if (L.use_fused) {
+    L.fused = align256(dfc::fused_workspace_bytes(c, B, H, W));
+    L.chunk = 1;  // fallback frames are re-run one at a time
+  } else {
+    L.fused = 0;
+    L.chunk = staged_chunk(B, H, W);
+  }
+  L.staged = staged_bytes(L.chunk > 0 ? L.chunk : 1, H, W);
+  L.total = L.fused + L.staged;
+  return L;
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+int dfc_abi_version(void) { return DFC_ABI_VERSION; }
+
+unsigned long long dfc_kernel_launches(void) { return dfc::g_kernel_launches.load(); }
+
+const char* dfc_last_error_string(void) { return g_err.c_str(); }
+
+int dfc_config_init(dfc_config* c) {
+  if (!c) return fail(DFC_E_INVALID, "null config");
+  std::memset(c, 0, sizeof(*c));
+  c->dilation_shape = DFC_SHAPE_DIAMOND;
+  c->dilation_size = 5;
+  c->closure_size = 5;
+  c->small_fill_size = 7;
+  c->large_fill_size = 31;
+  c->large_fill_max_iters = 100;
+  c->blur_mode = DFC_BLUR_MEDIAN_GAUSSIAN;
+  c->median_size = 5;
+  c->gaussian_size = 5;
+  c->bilateral_size = 5;
+  c->gaussian_sigma = 1.1;
+  c->bilateral_sigma_value = 1.5;
+  c->bilateral_sigma_space = 2.0;
+  c->fill_mode = DFC_FILL_FULL;
+  c->max_depth = 100.0f;
+  c->multiscale = 0;
+  c->bin_edge_near = 15.0f;
+  c->bin_edge_far = 30.0f;
+  c->near_shape = DFC_SHAPE_FULL;
+  c->near_size = 7;
+  c->med_shape = DFC_SHAPE_DIAMOND;
+  c->med_size = 7;
+  c->far_shape = DFC_SHAPE_DIAMOND;
+  c->far_size = 5;
+  c->flags = 0;
+  return DFC_OK;
+}
+
+size_t dfc_workspace_bytes(const dfc_config* cfg, int64_t B, int32_t H, int32_t W) {
+  if (!cfg || check_shape(B, H, W) != DFC_OK || check_config(*cfg) != DFC_OK) return 0;
+  const dfc_config c = fit_to_frame(*cfg, H, W);
+  return ws_layout(c, B, H, W).total;
+}
+
+int dfc_fill_batch(const float* in, float* out, int64_t B, int32_t H, int32_t W, const dfc_config* cfg,
+                   uint32_t* frame_status, int32_t* large_fill_iters, void* workspace, size_t ws_bytes,
+                   void* stream) {
+  if (!cfg) return fail(DFC_E_INVALID, "null config");
+  int rc = check_shape(B, H, W);
+  if (rc) return rc;
+  rc = check_config(*cfg);
+  if (rc) return rc;
+  if (B == 0) return DFC_OK;
+  if (!in || !out || !frame_status) return fail(DFC_E_INVALID, "null buffer");
+  const dfc_config c = fit_to_frame(*cfg, H, W);
+  const WsLayout L = ws_layout(c, B, H, W);
+  if (!workspace || ws_bytes < L.total)
+    return fail(DFC_E_WORKSPACE, "workspace too small: need " + std::to_string(L.total) + " bytes");
+  cudaStream_t s = as_stream(stream);
+  DFC_CK(cudaMemsetAsync(frame_status, 0, B * 4, s));
+  if (large_fill_iters) DFC_CK(cudaMemsetAsync(large_fill_iters, 0, B * 4, s));
+  if (!L.use_fused) {
+    return run_staged(in, out, B, H, W, c, frame_status, large_fill_iters, static_cast<char*>(workspace) + L.fused,
+                      L.staged, s);
+  }
+  DFC_CK(dfc::launch_fused(in, out, B, H, W, c, frame_status, large_fill_iters, workspace, L.fused, s));
+  if (c.flags & DFC_F_NO_FINISH) return DFC_OK;
+  return dfc_fill_finish(in, out, B, H, W, cfg, frame_status, large_fill_iters, workspace, ws_bytes, stream);
+}
+
+int dfc_fill_finish(const float* in, float* out, int64_t B, int32_t H, int32_t W, const dfc_config* cfg,
+                    uint32_t* frame_status, int32_t* large_fill_iters, void* workspace, size_t ws_bytes,
+                    void* stream) {
+  if (!cfg) return fail(DFC_E_INVALID, "null config");
+  const dfc_config c = fit_to_frame(*cfg, H, W);
+  const WsLayout L = ws_layout(c, B, H, W);
+  if (!L.use_fused || B == 0) return DFC_OK;
+  if (!workspace || ws_bytes < L.total) return fail(DFC_E_WORKSPACE, "workspace too small");
+  cudaStream_t s = as_stream(stream);
+  // fused.cu keeps a device counter of frames that need the staged path at the
+  // start of its workspace region.
+  unsigned long long nfb = 0;
+  DFC_CK(cudaMemcpyAsync(&nfb, workspace, 8, cudaMemcpyDeviceToHost, s));
+  DFC_CK(cudaStreamSynchronize(s));
+  if (nfb == 0) return DFC_OK;
+  std::vector<uint32_t> st(B);
+  DFC_CK(cudaMemcpyAsync(st.data(), frame_status, B * 4, cudaMemcpyDeviceToHost, s));
+  DFC_CK(cudaStreamSynchronize(s));
+  const int64_t HW = (int64_t)H * W;
+  for (int64_t b = 0; b < B; ++b) {
+    if (!(st[b] & 0x200u)) continue;  // internal "needs staged" bit set by the fused kernel
+    DFC_CK(cudaMemsetAsync(frame_status + b, 0, 4, s));
+    if (large_fill_iters) DFC_CK(cudaMemsetAsync(large_fill_iters + b, 0, 4, s));
+    int rc = run_staged(in + b * HW, out + b * HW, 1, H, W, c, frame_status + b,
+                        large_fill_iters ? large_fill_iters + b : nullptr, static_cast<char*>(workspace) + L.fused,
+                        L.staged, s);
+    if (rc) return rc;
+    DFC_CK(dfc::launch_or_status(frame_status + b, DFC_ST_FALLBACK, s));
+  }
+  return DFC_OK;
+}
+
+size_t dfc_op_workspace_bytes(int64_t B, int32_t H, int32_t W) { return (size_t)B * H * W * 8; }
+
+static int op_prologue(const void* in, const void* out, int64_t B, int32_t H, int32_t W) {
+  int rc = check_shape(B, H, W);
+  if (rc) return rc;
+  if (B > 0 && (!in || !out)) return fail(DFC_E_INVALID, "null buffer");
+  return DFC_OK;
+}
+
+static int box_op(const float* in, float* out, int64_t B, int32_t H, int32_t W, int32_t radius, void* ws,
+                  size_t wsb, void* stream, bool is_min) {
+  int rc = op_prologue(in, out, B, H, W);
+  if (rc || B == 0) return rc;
+  if (radius < 0) return fail(DFC_E_INVALID, "radius must be >= 0");
+  if (!ws || wsb < (size_t)B * H * W * 4) return fail(DFC_E_WORKSPACE, "workspace too small");
+  cudaStream_t s = as_stream(stream);
+  DFC_CK(dfc::launch_line_minmax(in, (float*)ws, B, H, W, radius, is_min, 1, s));
+  DFC_CK(dfc::launch_line_minmax((float*)ws, out, B, H, W, radius, is_min, 0, s));
+  return DFC_OK;
+}
+
+int dfc_box_max(const float* in, float* out, int64_t B, int32_t H, int32_t W, int32_t radius, void* ws, size_t wsb,
+                void* stream) {
+  return box_op(in, out, B, H, W, radius, ws, wsb, stream, false);
+}
+
+int dfc_box_min(const float* in, float* out, int64_t B, int32_t H, int32_t W, int32_t radius, void* ws, size_t wsb,
+                void* stream) {
+  return box_op(in, out, B, H, W, radius, ws, wsb, stream, true);
+}
+
+static int offs_op(const float* in, float* out, int64_t B, int32_t H, int32_t W, const int32_t* offsets, int32_t n,
+                   void* stream, bool is_min) {
+  int rc = op_prologue(in, out, B, H, W);
+  if (rc || B == 0) return rc;
+  if (!offsets || n < 1) return fail(DFC_E_INVALID, "empty offset list");
+  if (n > 4096) return fail(DFC_E_UNSUPPORTED, "more than 4096 offsets");
+  for (int t = 0; t < 2 * n; ++t)
+    if (offsets[t] < -127 || offsets[t] > 127) return fail(DFC_E_UNSUPPORTED, "offset magnitude > 127");
+  DFC_CK(dfc::launch_offsets_minmax(in, out, B, H, W, offsets, n, is_min, as_stream(stream)));
+  return DFC_OK;
+}
+
+int dfc_offsets_max(const float* in, float* out, int64_t B, int32_t H, int32_t W, const int32_t* offsets,
+                    int32_t n, void* stream) {
+  return offs_op(in, out, B, H, W, offsets, n, stream, false);
+}
+
+int dfc_offsets_min(const float* in, float* out, int64_t B, int32_t H, int32_t W, const int32_t* offsets,
+                    int32_t n, void* stream) {
+  return offs_op(in, out, B, H, W, offsets, n, stream, true);
+}
+
+int dfc_median(const float* in, float* out, int64_t B, int32_t H, int32_t W, int32_t size, void* stream) {
+  int rc = op_prologue(in, out, B, H, W);
+  if (rc || B == 0) return rc;
+  if (!odd3(size)) return fail(DFC_E_INVALID, "window size must be odd and >= 3, got " + std::to_string(size));
+  DFC_CK(dfc::launch_median(in, out, B, H, W, size, as_stream(stream)));
+  return DFC_OK;
+}
+
+int dfc_gaussian_separable(const float* in, float* out, int64_t B, int32_t H, int32_t W, const double* weights,
+                           int32_t k, int32_t exact, void* ws, size_t wsb, void* stream) {
+  int rc = op_prologue(in, out, B, H, W);
+  if (rc || B == 0) return rc;
+  if (!weights || k < 1 || k > 64) return fail(DFC_E_INVALID, "weights must have 1..64 taps");
+  const size_t need = (size_t)B * H * W * (exact ? 8 : 4);
+  if (!ws || wsb < need) return fail(DFC_E_WORKSPACE, "workspace too small");
+  cudaStream_t s = as_stream(stream);
+  DFC_CK(dfc::launch_gauss_line(in, ws, B, H, W, weights, k, 1, exact != 0, false, exact != 0, s));
+  DFC_CK(dfc::launch_gauss_line((const float*)ws, out, B, H, W, weights, k, 0, exact != 0, exact != 0, false, s));
+  return DFC_OK;
+}
+
+int dfc_bilateral(const float* in, float* out, int64_t B, int32_t H, int32_t W, int32_t size, double sigma_value,
+                  double sigma_space, int32_t exact, void* stream) {
+  int rc = op_prologue(in, out, B, H, W);
+  if (rc || B == 0) return rc;
+  if (!odd3(size)) return fail(DFC_E_INVALID, "window size must be odd and >= 3, got " + std::to_string(size));
+  if (!(sigma_value > 0) || !(sigma_space > 0)) return fail(DFC_E_INVALID, "bilateral sigmas must be positive");
+  DFC_CK(dfc::launch_bilateral(in, out, B, H, W, size, sigma_value, sigma_space, exact != 0, as_stream(stream)));
+  return DFC_OK;
+}
+
+int dfc_invert(const float* in, float* out, int64_t B, int32_t H, int32_t W, float offset, uint32_t* frame_status,
+               void* stream) {
+  int rc = op_prologue(in, out, B, H, W);
+  if (rc || B == 0) return rc;
+  DFC_CK(dfc::launch_invert(in, out, (int64_t)H * W, B, offset, frame_status, as_stream(stream)));
+  return DFC_OK;
+}
+
+int dfc_validate(const float* in, int64_t B, int32_t H, int32_t W, uint32_t* frame_status, int64_t* n_valid,
+                 void* stream) {
+  int rc = op_prologue(in, frame_status, B, H, W);
+  if (rc || B == 0) return rc;
+  cudaStream_t s = as_stream(stream);
+  if (n_valid) {
+    DFC_CK(cudaMemsetAsync(n_valid, 0, B * 8, s));
+  }
+  DFC_CK(dfc::launch_validate(in, (int64_t)H * W, B, frame_status, n_valid, s));
+  if (n_valid) DFC_CK(dfc::launch_finalize_status(n_valid, frame_status, B, s));
+  return DFC_OK;
+}
+
+int dfc_masked_fill(const float* cur, const float* dilated, float* out, int64_t B, int32_t H, int32_t W,
+                    void* stream) {
+  int rc = op_prologue(cur, out, B, H, W);
+  if (rc || B == 0) return rc;
+  if (!dilated) return fail(DFC_E_INVALID, "null buffer");
+  DFC_CK(dfc::launch_masked_fill(cur, dilated, out, B * H * (int64_t)W, as_stream(stream)));
+  return DFC_OK;
+}
+
+int dfc_extend_to_top(const float* in, float* out, int64_t B, int32_t H, int32_t W, void* stream) {
+  int rc = op_prologue(in, out, B, H, W);
+  if (rc || B == 0) return rc;
+  if (in == out) return fail(DFC_E_INVALID, "extend_to_top cannot run in place");
+  DFC_CK(dfc::launch_extend_to_top(in, out, B, H, W, as_stream(stream)));
+  return DFC_OK;
+}
+
+int dfc_count_empty(const float* in, int64_t B, int32_t H, int32_t W, int64_t* counts, void* stream) {
+  int rc = op_prologue(in, counts, B, H, W);
+  if (rc || B == 0) return rc;
+  cudaStream_t s = as_stream(stream);
+  DFC_CK(cudaMemsetAsync(counts, 0, B * 8, s));
+  DFC_CK(dfc::launch_count_empty(in, (int64_t)H * W, B, counts, s));
+  return DFC_OK;
+}
+
+int dfc_reimpose(const float* blurred, const float* mask_src, float* out, int64_t B, int32_t H, int32_t W,
+                 void* stream) {
+  int rc = op_prologue(blurred, out, B, H, W);
+  if (rc || B == 0) return rc;
+  if (!mask_src) return fail(DFC_E_INVALID, "null buffer");
+  DFC_CK(dfc::launch_reimpose(blurred, mask_src, out, B * H * (int64_t)W, as_stream(stream)));
+  return DFC_OK;
+}
+
+}  // extern "C"

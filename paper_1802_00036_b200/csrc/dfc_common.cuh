@@ -1,0 +1,68 @@
+// Shared device helpers and internal launcher declarations for libdfc.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+
+#include "dfc.h"
+
+namespace dfc {
+
+// Validity threshold: the reference compares float32 maps against the
+// Python float 0.1, which numpy-2 evaluates as float32(0.1) = 0x3DCCCCCD
+// (depth_core.py:20,151).
+constexpr float kValid = 0.1f;
+
+__device__ __forceinline__ bool is_valid(float v) { return v > kValid; }
+__device__ __forceinline__ int clampi(int i, int n) { return i < 0 ? 0 : (i >= n ? n - 1 : i); }
+__device__ __forceinline__ float max3(float a, float b, float c) { return fmaxf(fmaxf(a, b), c); }
+__device__ __forceinline__ float min3(float a, float b, float c) { return fminf(fminf(a, b), c); }
+
+struct MaxOp {
+  static __device__ __forceinline__ float identity() { return 0.0f; }  // all maps are >= 0
+  static __device__ __forceinline__ float apply(float a, float b) { return fmaxf(a, b); }
+};
+struct MinOp {
+  static __device__ __forceinline__ float identity() { return 3.402823466e38f; }
+  static __device__ __forceinline__ float apply(float a, float b) { return fminf(a, b); }
+};
+
+// process-wide count of kernels launched by libdfc (diagnostics for the bench)
+extern std::atomic<unsigned long long> g_kernel_launches;
+inline void note_launch(unsigned long long n = 1) { g_kernel_launches.fetch_add(n, std::memory_order_relaxed); }
+
+// ---- internal launchers (ops_kernels.cu) ---------------------------------
+cudaError_t launch_line_minmax(const float* in, float* out, int64_t B, int H, int W, int radius, bool is_min,
+                               int axis, cudaStream_t s);
+cudaError_t launch_offsets_minmax(const float* in, float* out, int64_t B, int H, int W, const int32_t* offs, int n,
+                                  bool is_min, cudaStream_t s);
+cudaError_t launch_median(const float* in, float* out, int64_t B, int H, int W, int size, cudaStream_t s);
+cudaError_t launch_gauss_line(const float* in, void* out, int64_t B, int H, int W, const double* w, int k,
+                              int axis, bool exact, bool in_is_f64, bool out_is_f64, cudaStream_t s);
+cudaError_t launch_bilateral(const float* in, float* out, int64_t B, int H, int W, int size, double sv, double ss,
+                             bool exact, cudaStream_t s);
+cudaError_t launch_invert(const float* in, float* out, int64_t n_per_frame, int64_t B, float offset,
+                          uint32_t* status, cudaStream_t s);
+cudaError_t launch_validate(const float* in, int64_t n_per_frame, int64_t B, uint32_t* status, int64_t* n_valid,
+                            cudaStream_t s);
+cudaError_t launch_masked_fill(const float* cur, const float* dil, float* out, int64_t n, cudaStream_t s);
+cudaError_t launch_extend_to_top(const float* in, float* out, int64_t B, int H, int W, cudaStream_t s);
+cudaError_t launch_count_empty(const float* in, int64_t n_per_frame, int64_t B, int64_t* counts, cudaStream_t s);
+cudaError_t launch_reimpose(const float* blurred, const float* mask_src, float* out, int64_t n, cudaStream_t s);
+cudaError_t launch_bin_select(const float* direct, const float* inv, float* out, int64_t n, float lo, float hi,
+                              cudaStream_t s);
+cudaError_t launch_max2(const float* a, const float* b, float* out, int64_t n, cudaStream_t s);
+cudaError_t launch_iter_update(const int64_t* counts, int32_t* iters, int64_t B, unsigned long long* total,
+                               cudaStream_t s);
+cudaError_t launch_or_status(uint32_t* status, uint32_t bits, cudaStream_t s);
+cudaError_t launch_finalize_status(const int64_t* n_valid, uint32_t* status, int64_t B, cudaStream_t s);
+
+// ---- fused pipeline (fused.cu) -------------------------------------------
+struct FusedPlan;
+bool fused_supported(const dfc_config& c, int H, int W);
+size_t fused_workspace_bytes(const dfc_config& c, int64_t B, int H, int W);
+cudaError_t launch_fused(const float* in, float* out, int64_t B, int H, int W, const dfc_config& c,
+                         uint32_t* status, int32_t* iters, void* ws, size_t ws_bytes, cudaStream_t s);
+
+}  // namespace dfc

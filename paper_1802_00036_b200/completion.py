@@ -194,7 +194,10 @@ def complete_batch(frames, config: PipelineConfig | None = None, multiscale: Mul
     """Complete a [B, H, W] batch (torch CUDA tensor, or host array copied in)."""
     config = config or PipelineConfig()
     if isinstance(frames, np.ndarray):
-        frames = torch.from_numpy(np.ascontiguousarray(frames, dtype=np.float32))
+        frames = np.ascontiguousarray(frames, dtype=np.float32)
+        if not frames.flags.writeable:
+            frames = frames.copy()
+        frames = torch.from_numpy(frames)
     if frames.device.type != "cuda":
         frames = frames.to(_device(), non_blocking=True)
     if frames.dim() == 2:

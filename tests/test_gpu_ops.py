@@ -132,8 +132,10 @@ def test_invert_range_and_validate(ops):
     x[2, 0, 0] = np.inf
     st, nv = ops.validate(_dev(x))
     st = st.cpu().tolist()
-    assert st[0] == 0 and st[1] == 2 and st[2] & 1 and st[2] & 4
-    assert nv.cpu().tolist() == [1, 1, 0]
+    assert st[0] == 0 and st[1] == 2 and st[2] == 1  # inf > 0.1 counts as "valid" (pipeline.py:138)
+    assert nv.cpu().tolist() == [1, 1, 1]
+    st, nv = ops.validate(_dev(np.zeros((2, 3, 3), np.float32)))
+    assert st.cpu().tolist() == [4, 4] and nv.cpu().tolist() == [0, 0]
 
 
 def test_count_empty_and_reimpose(ops):

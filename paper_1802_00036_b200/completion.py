@@ -260,7 +260,7 @@ def complete_with_stats(sparse, config: PipelineConfig | None = None) -> tuple[D
     if sparse.encoding is not DepthEncoding.DIRECT:
         raise EncodingError("pipeline input must be direct-encoded")
     dev = _device()
-    x = torch.from_numpy(np.ascontiguousarray(sparse.values)).to(dev)
+    x = torch.from_numpy(np.array(sparse.values, dtype=np.float32, copy=True)).to(dev)
     n_valid = int(np.count_nonzero(sparse.values > np.float32(domain.VALIDITY_THRESHOLD)))
     if n_valid == 0:
         raise DegenerateInputError("input depth map has no valid pixels")

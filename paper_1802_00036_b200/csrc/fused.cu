@@ -1,33 +1,36 @@
 // Fused streaming depth-completion kernel for sm_100a (the hot path).
 //
 // One persistent CTA works on one (frame, column strip) item at a time; a
-// strip is the whole frame for W <= 1248.  Warps own 104-column slices with
+// strip is the whole frame for W <= 1248.  Warps own ~104-column slices with
 // 12-column lane halos (32 lanes x 4 columns = 128 columns per warp), so all
-// horizontal neighbour traffic is warp shuffles and warps never wait on each
-// other except at one CTA barrier per 4-row block.
+// horizontal neighbour traffic is warp shuffles and warps meet only at one
+// CTA barrier per 4-row block.  Columns outside the frame (one lane at the
+// left frame edge, >= 1 lane at the right edge) carry neutral values through
+// the min/max stages and replicated values into the blur, which reproduces
+// the reference's replicate border exactly.
 //
-// Phase 1 (FULL mode, extend_to_top needs each column's first valid row r0):
-//   top-down over 32-row blocks, validity bit-packed in 64-bit column words;
-//   the stage-4 validity equals the binary morphology D7(E5(D5(D_shape(M0))))
-//   of the input mask (SURVEY.md App. B probe 13), so r0 comes from bitwise
-//   ops only.  The scan stops as soon as every owned column has its r0.
-// Phase 2: bottom-up streaming in 4-row blocks.  Going up, a column's r0 row
-//   is met before the rows above it, so extend_to_top needs no look-ahead.
+// Phase 1 (FULL mode: extend_to_top needs each column's first valid row r0):
+//   top-down over 32-row blocks, validity bit-packed in 64-bit column words.
+//   The stage-4 validity equals the binary morphology D7(E5(D5(D_shape(M0))))
+//   of the input mask (SURVEY.md App. B probe 13), so r0 needs bit ops only.
+//   The scan stops once every owned column has its r0.
+// Phase 2: bottom-up streaming in 4-row blocks (going up, a column's r0 row
+//   comes before the rows above it, so extend_to_top needs no look-ahead).
 //   Producer (registers + shuffles): invert -> cross3 -> cross3 (= 5x5
 //   diamond) -> max5 -> min5 (close) -> masked max7 (small fill) -> extend.
 //   Stage-5 rows go to a 40-row shared-memory ring; the consumer runs 16 rows
-//   behind: large 31x31 masked fill (only where empties exist, warp-
-//   cooperative), Gaussian 5x5 (fp32), invert back, one coalesced store.
-//   Rows above every owned column's r0 + 9 need no stage 1-4 work and no
-//   input read: they become the captured top values directly.
-// Frames that still hold empties after one large-fill iteration (never on
-// KITTI-like data) are flagged and re-run by the staged path (capi.cu).
+//   behind: 31x31 masked large fill (warp-cooperative, only for blocks that
+//   hold an empty pixel), 5x5 Gaussian (fp32), invert back, coalesced store.
+//   Once the stage-5 rows are above every owned column's r0, stages 1-4 and
+//   the input reads stop: those rows are the captured top values.
+// Frames that still hold empties after one large-fill iteration are flagged
+// for the staged path (capi.cu: dfc_fill_finish).
 //
 // Reference semantics: depth_core.py:150-156 (invert), morphology.py:39-96
-// (dilate/close/masked fill/extend), pipeline.py:154-214 (stage order, fill
-// loop, blur, partial re-impose).  Exactness notes: all selection stages are
-// bit-exact by construction (min/max with clipped windows == replicate);
-// the Gaussian is fp32 (<= 1e-4 m vs the fp64 reference, tested).
+// (dilate / close / masked fill / extend), pipeline.py:154-214 (stage order,
+// fill loop, blur, partial re-impose).  Every selection stage is bit-exact by
+// construction (min/max over clipped windows == replicate border); the
+// Gaussian is fp32 (<= 1e-4 m against the fp64 reference; tested).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -42,18 +45,21 @@ namespace {
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kNW = 12;                // warps per CTA
 constexpr int kLW = 128;               // columns per warp (32 lanes x 4)
-constexpr int kHalo = 12;              // lane-halo columns per side (>= 9 morphology + 2 blur + 1)
-constexpr int kOwn = kLW - 2 * kHalo;  // 104
+constexpr int kHalo = 12;              // lane-halo columns per side (9 morphology + 2 blur, lane aligned)
 constexpr int kB = 4;                  // rows per block
 constexpr int kRing = 40;              // stage-5 ring rows (39 live)
+constexpr int kRingBlocks = kRing / kB;
 constexpr int kLag = 16;               // consumer lag behind the stage-5 producer (>= 15)
 constexpr int kPLag = 9;               // stage-5 lag behind the input: 1+1+2+2+3
-constexpr int kCLag = kPLag + kLag;    // 25: consumer rows = t0 - 25 + j
+constexpr int kCLag = kPLag + kLag;    // consumer rows = t0 - 25 + j
+constexpr int kKFirst = (kCLag - 1 + kB - 1) / kB;  // first consumer block (needs rows <= +15 produced)
 constexpr int kVC = 160;               // large-fill scratch columns per warp (128 + 2*15, padded)
 constexpr int kLF = 15;                // large fill radius
 constexpr int kStripMax = 1248;        // widest strip handled by one CTA
 constexpr float kFMax = 3.402823466e38f;
 constexpr uint32_t kNeedsStaged = 0x200u;  // internal status bit (capi.cu)
+
+static_assert(kRing % kB == 0 && kLag % kB == 0, "ring blocks must not wrap inside a block");
 
 struct F4 {
   float v[4];
@@ -63,7 +69,7 @@ struct Params {
   const float* in;
   float* out;
   int64_t nframes;
-  int H, W, strips, SW;
+  int H, W, strips, SW, nw;
   float md;
   float gw[5];
   uint32_t* status;
@@ -74,46 +80,42 @@ struct Params {
 };
 
 // ---------------------------------------------------------------------------
-// small helpers
+// helpers
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ float fmx(float a, float b) { return fmaxf(a, b); }
 __device__ __forceinline__ float fmx3(float a, float b, float c) { return fmaxf(fmaxf(a, b), c); }
-__device__ __forceinline__ float fmn(float a, float b) { return fminf(a, b); }
 __device__ __forceinline__ float fmn3(float a, float b, float c) { return fminf(fminf(a, b), c); }
 
 struct OpMax {
-  static __device__ __forceinline__ float f(float a, float b) { return fmx(a, b); }
+  static __device__ __forceinline__ float f(float a, float b) { return fmaxf(a, b); }
   static __device__ __forceinline__ float f3(float a, float b, float c) { return fmx3(a, b, c); }
 };
 struct OpMin {
-  static __device__ __forceinline__ float f(float a, float b) { return fmn(a, b); }
+  static __device__ __forceinline__ float f(float a, float b) { return fminf(a, b); }
   static __device__ __forceinline__ float f3(float a, float b, float c) { return fmn3(a, b, c); }
 };
 
-// Row extended by R columns each side: e[i] <-> column x0 - R + i.  Lane 0
-// and lane 31 replicate their own edge column: exact at a frame edge (clipped
-// window == replicate) and harmless in halo lanes.
+// Row extended by R columns each side: e[i] <-> column x0 - R + i.  Lanes 0
+// and 31 read their own registers for the missing neighbour; both are halo
+// or out-of-frame lanes whose results are never used.
 template <int R>
 struct Ext {
   float e[4 + 2 * R];
 };
 
 template <int R>
-__device__ __forceinline__ Ext<R> ext_row(const F4& a, int lane) {
+__device__ __forceinline__ Ext<R> ext_row(const F4& a) {
   Ext<R> o;
 #pragma unroll
   for (int i = 0; i < R; ++i) {
-    const float l = __shfl_up_sync(kFull, a.v[3 - i], 1);
-    const float r = __shfl_down_sync(kFull, a.v[i], 1);
-    o.e[R - 1 - i] = lane == 0 ? a.v[0] : l;
-    o.e[R + 4 + i] = lane == 31 ? a.v[3] : r;
+    o.e[R - 1 - i] = __shfl_up_sync(kFull, a.v[3 - i], 1);
+    o.e[R + 4 + i] = __shfl_down_sync(kFull, a.v[i], 1);
   }
 #pragma unroll
   for (int i = 0; i < 4; ++i) o.e[R + i] = a.v[i];
   return o;
 }
 
-// horizontal windows (shared sub-results across the lane's 4 columns)
 template <class Op>
 __device__ __forceinline__ F4 hwin2(const Ext<2>& x) {
   F4 o;
@@ -129,17 +131,15 @@ template <class Op>
 __device__ __forceinline__ F4 hwin3(const Ext<3>& x) {
   F4 o;
   const float q = Op::f(Op::f3(x.e[3], x.e[4], x.e[5]), x.e[6]);
-  const float a1 = Op::f3(x.e[0], x.e[1], x.e[2]);
   const float b = Op::f(x.e[1], x.e[2]);
   const float c2 = Op::f(x.e[7], x.e[8]);
-  o.v[0] = Op::f(q, a1);
+  o.v[0] = Op::f3(q, b, x.e[0]);
   o.v[1] = Op::f3(q, b, x.e[7]);
   o.v[2] = Op::f3(q, x.e[2], c2);
   o.v[3] = Op::f3(q, c2, x.e[9]);
   return o;
 }
 
-// vertical windows over a block array in[kB + 2R] -> out[kB]
 template <class Op>
 __device__ __forceinline__ void vwin2(const F4* in, F4* out) {
 #pragma unroll
@@ -159,10 +159,9 @@ __device__ __forceinline__ void vwin3(const F4* in, F4* out) {
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
     const float q = Op::f(Op::f3(in[3].v[c], in[4].v[c], in[5].v[c]), in[6].v[c]);
-    const float a1 = Op::f3(in[0].v[c], in[1].v[c], in[2].v[c]);
     const float b = Op::f(in[1].v[c], in[2].v[c]);
     const float c2 = Op::f(in[7].v[c], in[8].v[c]);
-    out[0].v[c] = Op::f(q, a1);
+    out[0].v[c] = Op::f3(q, b, in[0].v[c]);
     out[1].v[c] = Op::f3(q, b, in[7].v[c]);
     out[2].v[c] = Op::f3(q, in[2].v[c], c2);
     out[3].v[c] = Op::f3(q, c2, in[9].v[c]);
@@ -174,7 +173,6 @@ __device__ __forceinline__ void set_row(F4& a, float v) {
   for (int c = 0; c < 4; ++c) a.v[c] = v;
 }
 
-// OOB columns (>= W) of the lane get `v` (edge warps only; mask is per lane)
 __device__ __forceinline__ void fix_oob(F4& a, unsigned oob, float v) {
 #pragma unroll
   for (int c = 0; c < 4; ++c)
@@ -184,24 +182,26 @@ __device__ __forceinline__ void fix_oob(F4& a, unsigned oob, float v) {
 // ---------------------------------------------------------------------------
 // global memory access for one lane's 4 columns of a row
 // ---------------------------------------------------------------------------
-template <int VEC>
+template <int VEC, bool STREAM>
 __device__ __forceinline__ F4 load4(const float* row, int x0, int W) {
   F4 r;
-  if (x0 + 3 < W) {
+  if (x0 >= 0 && x0 + 3 < W) {
     if constexpr (VEC == 4) {
-      const float4 t = __ldcs(reinterpret_cast<const float4*>(row + x0));
+      const float4* a = reinterpret_cast<const float4*>(row + x0);
+      const float4 t = STREAM ? __ldcs(a) : __ldg(a);
       r.v[0] = t.x, r.v[1] = t.y, r.v[2] = t.z, r.v[3] = t.w;
     } else if constexpr (VEC == 2) {
-      const float2 a = __ldcs(reinterpret_cast<const float2*>(row + x0));
-      const float2 b = __ldcs(reinterpret_cast<const float2*>(row + x0 + 2));
-      r.v[0] = a.x, r.v[1] = a.y, r.v[2] = b.x, r.v[3] = b.y;
+      const float2* a = reinterpret_cast<const float2*>(row + x0);
+      const float2 u = STREAM ? __ldcs(a) : __ldg(a);
+      const float2 w = STREAM ? __ldcs(a + 1) : __ldg(a + 1);
+      r.v[0] = u.x, r.v[1] = u.y, r.v[2] = w.x, r.v[3] = w.y;
     } else {
 #pragma unroll
-      for (int c = 0; c < 4; ++c) r.v[c] = __ldcs(row + x0 + c);
+      for (int c = 0; c < 4; ++c) r.v[c] = STREAM ? __ldcs(row + x0 + c) : __ldg(row + x0 + c);
     }
   } else {
 #pragma unroll
-    for (int c = 0; c < 4; ++c) r.v[c] = (x0 + c < W) ? __ldcs(row + x0 + c) : 0.0f;
+    for (int c = 0; c < 4; ++c) r.v[c] = (x0 + c >= 0 && x0 + c < W) ? __ldg(row + x0 + c) : 0.0f;
   }
   return r;
 }
@@ -226,40 +226,40 @@ __device__ __forceinline__ void store4(float* row, int x0, const F4& a, unsigned
 // ---------------------------------------------------------------------------
 // per-item warp geometry
 // ---------------------------------------------------------------------------
-struct WarpGeo {
-  int L;       // first lane column of this warp
-  int q0, q1;  // stage-5 owned columns (ring writer)
-  int nw;      // warps used by this item
+struct Geo {
+  int o0, o1;  // output columns of the strip
+  int p0, p1;  // stage-5 production (ring) columns
+  int L;       // first lane column of this warp (-4 at the left frame edge)
+  int q0, q1;  // stage-5 columns this warp owns (writes to the ring); empty for spare warps
 };
 
-__device__ void item_geometry(int s, const Params& p, int warp, int& o0, int& o1, int& p0, int& p1, WarpGeo& g) {
-  o0 = s * p.SW;
-  o1 = min(p.W, o0 + p.SW);
-  p0 = o0 == 0 ? 0 : max(0, (o0 - 17) & ~3);
-  p1 = o1 == p.W ? p.W : min(p.W, (o1 + 17 + 3) & ~3);
-  int q0 = p0, nw = 0;
-  g.L = 0;
-  g.q0 = g.q1 = 0;
-  while (q0 < p1) {
-    const int L = q0 == 0 ? 0 : q0 - kHalo;
-    int q1;
-    if (p1 == p.W && L + kLW >= p.W)
-      q1 = p.W;
-    else
-      q1 = min(p1, (L == 0 ? kLW - kHalo : q0 + kOwn));
-    if (nw == warp) {
-      g.L = L;
-      g.q0 = q0;
-      g.q1 = q1;
+__device__ __forceinline__ int warp_q1(int L, int q0, int p1, int W) {
+  if (p1 == W && L + kLW - 4 >= W) return W;  // right frame edge, >= 1 out-of-frame lane
+  return min(p1, L + kLW - kHalo);
+}
+
+__device__ void item_geometry(int s, const Params& p, int warp, Geo& g) {
+  g.o0 = s * p.SW;
+  g.o1 = min(p.W, g.o0 + p.SW);
+  g.p0 = g.o0 == 0 ? 0 : max(0, (g.o0 - 17) & ~3);
+  g.p1 = g.o1 == p.W ? p.W : min(p.W, (g.o1 + 17 + 3) & ~3);
+  int q0 = g.p0, L = 0, q1 = 0;
+  for (int w = 0; w <= warp; ++w) {
+    if (q0 >= g.p1) {  // spare warp: duplicate the last one, own nothing
+      q0 = q1 = g.p1;
+      break;
     }
-    ++nw;
-    q0 = q1;
+    L = q0 == 0 ? -4 : q0 - kHalo;
+    q1 = warp_q1(L, q0, g.p1, p.W);
+    if (w < warp) q0 = q1;
   }
-  g.nw = nw;
+  g.L = L;
+  g.q0 = q0;
+  g.q1 = q1;
 }
 
 // ---------------------------------------------------------------------------
-// Phase 1: first valid stage-4 row per column from bit-packed morphology
+// Phase 1: first valid stage-4 row per column, bit-packed morphology
 // ---------------------------------------------------------------------------
 template <int VEC>
 __device__ __forceinline__ void load_bits(const float* frame, int H, int W, int x0, int y0, float md, uint32_t w[4],
@@ -267,18 +267,25 @@ __device__ __forceinline__ void load_bits(const float* frame, int H, int W, int 
 #pragma unroll
   for (int c = 0; c < 4; ++c) w[c] = 0;
   if (y0 >= H) return;
-#pragma unroll 8
-  for (int i = 0; i < 32; ++i) {
-    const int y = y0 + i;
-    if (y < H) {
-      const F4 v = load4<VEC>(frame + (int64_t)y * W, x0, W);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    F4 v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int y = y0 + 16 * h + i;
+      if (y < H)
+        v[i] = load4<VEC, false>(frame + (int64_t)y * W, x0, W);
+      else
+        set_row(v[i], 0.f);
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        umax = max(umax, __float_as_uint(v.v[c]));
-        const float inv = v.v[c] > kValid ? md - v.v[c] : 0.0f;
-        w[c] |= (uint32_t)(inv > kValid) << i;
+        umax = max(umax, __float_as_uint(v[i].v[c]));
+        const float inv = v[i].v[c] > kValid ? md - v[i].v[c] : 0.0f;
+        w[c] |= (uint32_t)(inv > kValid) << (16 * h + i);
       }
-    }
   }
 }
 
@@ -294,16 +301,13 @@ __device__ __forceinline__ uint64_t vero(uint64_t x, int r) {
   return o;
 }
 
-// horizontal OR / AND over +-R neighbouring column words; OOB words = oobv
 template <int R, bool AND>
-__device__ __forceinline__ void hcomb(const uint64_t in[4], uint64_t out[4], int lane, uint64_t oobv) {
+__device__ __forceinline__ void hcomb(const uint64_t in[4], uint64_t out[4]) {
   uint64_t e[4 + 2 * R];
 #pragma unroll
   for (int i = 0; i < R; ++i) {
-    const uint64_t l = __shfl_up_sync(kFull, in[3 - i], 1);
-    const uint64_t r = __shfl_down_sync(kFull, in[i], 1);
-    e[R - 1 - i] = lane == 0 ? oobv : l;
-    e[R + 4 + i] = lane == 31 ? oobv : r;
+    e[R - 1 - i] = __shfl_up_sync(kFull, in[3 - i], 1);
+    e[R + 4 + i] = __shfl_down_sync(kFull, in[i], 1);
   }
 #pragma unroll
   for (int i = 0; i < 4; ++i) e[R + i] = in[i];
@@ -317,54 +321,48 @@ __device__ __forceinline__ void hcomb(const uint64_t in[4], uint64_t out[4], int
 }
 
 template <int VEC>
-__device__ void phase1(const float* frame, const Params& p, int x0, int lane, bool needed, unsigned incol,
-                       int T0[4], unsigned& umax) {
+__device__ __forceinline__ void phase1(const float* frame, const Params& p, int x0, bool needed, unsigned incol,
+                                       int T0[4], unsigned& umax) {
   const int H = p.H, W = p.W;
   uint32_t prv[4] = {0, 0, 0, 0}, cur[4], nxt[4];
   load_bits<VEC>(frame, H, W, x0, 0, p.md, cur, umax);
   load_bits<VEC>(frame, H, W, x0, 32, p.md, nxt, umax);
   int r0[4] = {-1, -1, -1, -1};
+  uint64_t cm[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) cm[c] = (incol >> c & 1) ? ~0ull : 0ull;
   for (int b = 0; 32 * b < H; ++b) {
     uint64_t X[4], A[4], Bq[4];
-#pragma unroll
-    for (int c = 0; c < 4; ++c)
-      X[c] = (uint64_t)(prv[c] >> 16) | ((uint64_t)cur[c] << 16) | ((uint64_t)nxt[c] << 48);
-    // rows of the 64-bit window inside the frame
     const int lo = max(0, 16 - 32 * b), hi = min(64, H - 32 * b + 16);
     const uint64_t inrow = (hi <= lo) ? 0ull : ((hi - lo == 64) ? ~0ull : (((1ull << (hi - lo)) - 1) << lo));
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      X[c] = ((uint64_t)(prv[c] >> 16) | ((uint64_t)cur[c] << 16) | ((uint64_t)nxt[c] << 48)) & cm[c];
     // D_shape = cross3 o cross3 (5x5 diamond)
 #pragma unroll
     for (int it = 0; it < 2; ++it) {
-      hcomb<1, false>(X, A, lane, 0ull);
+      hcomb<1, false>(X, A);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        // cross: vertical 3 on the centre column | horizontal neighbours of the original row
-        const uint64_t v = vdil(X[c], 1) | A[c];
-        Bq[c] = (incol >> c & 1) ? (v & inrow) : 0ull;
-      }
+      for (int c = 0; c < 4; ++c) Bq[c] = (vdil(X[c], 1) | A[c]) & inrow & cm[c];
 #pragma unroll
       for (int c = 0; c < 4; ++c) X[c] = Bq[c];
     }
-    // D5 (close, dilate)
+    // D5
 #pragma unroll
     for (int c = 0; c < 4; ++c) A[c] = vdil(X[c], 2);
-    hcomb<2, false>(A, Bq, lane, 0ull);
+    hcomb<2, false>(A, Bq);
+    // E5: outside the frame counts as set (clipped window)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) X[c] = (incol >> c & 1) ? (Bq[c] & inrow) : 0ull;
-    // E5 (close, erode): outside the frame counts as set (clipped window)
+    for (int c = 0; c < 4; ++c) A[c] = vero((Bq[c] & inrow & cm[c]) | ~(inrow & cm[c]), 2);
+    hcomb<2, true>(A, Bq);
+    // D7
 #pragma unroll
-    for (int c = 0; c < 4; ++c) A[c] = vero((incol >> c & 1) ? (X[c] | ~inrow) : ~0ull, 2);
-    hcomb<2, true>(A, Bq, lane, ~0ull);
-#pragma unroll
-    for (int c = 0; c < 4; ++c) X[c] = (incol >> c & 1) ? (Bq[c] & inrow) : 0ull;
-    // D7 (small fill: valid | any valid within 7x7)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) A[c] = vdil(X[c], 3);
-    hcomb<3, false>(A, Bq, lane, 0ull);
+    for (int c = 0; c < 4; ++c) A[c] = vdil(Bq[c] & inrow & cm[c], 3);
+    hcomb<3, false>(A, Bq);
     bool done = true;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      const uint32_t cand = (uint32_t)(((incol >> c & 1) ? (Bq[c] & inrow) : 0ull) >> 16);
+      const uint32_t cand = (uint32_t)((Bq[c] & inrow & cm[c]) >> 16);
       if (r0[c] < 0 && cand) r0[c] = 32 * b + __ffs(cand) - 1;
       done = done && (r0[c] >= 0 || !(incol >> c & 1));
     }
@@ -381,51 +379,331 @@ __device__ void phase1(const float* frame, const Params& p, int x0, int lane, bo
 }
 
 // ---------------------------------------------------------------------------
-// Large masked fill for one consumer block (warp-cooperative, only when the
-// block holds an empty stage-5 pixel).  V[j][col] = max over rows
-// [r_j - 15, r_j + 15] (clamped == clipped for max) of the stage-5 ring;
-// then each empty pixel takes max over V[j][x-15 .. x+15].
+// Large masked fill, step A (warp-cooperative): V[j][sc] = max over ring rows
+// [c_j - 15, c_j + 15] (clamped == clipped for max) at column L - 15 + sc.
+// Consecutive centres c_j = c0 + j share rows [c0-12, c0+15].
 // ---------------------------------------------------------------------------
-__device__ __noinline__ void large_fill_vstep(const float* __restrict__ ring, int ringw, int p0, int p1, int H,
-                                              int L, int lane, int tc0, float* __restrict__ V) {
-  // 160 scratch columns starting at L - 15; lane handles 5 of them
+__device__ __noinline__ void lf_vstep(const float* __restrict__ ring, int ringw, int p0, int p1, int H, int L,
+                                      int lane, int c0, bool consecutive, float* __restrict__ V) {
 #pragma unroll 1
   for (int i = 0; i < kVC / 32; ++i) {
     const int sc = lane + 32 * i;
     const int col = L - kLF + sc;
-    float o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
+    float o[4] = {0.f, 0.f, 0.f, 0.f};
     if (col >= p0 && col < p1) {
       const float* rc = ring + (col - p0);
       auto ld = [&](int r) {
         const int rr = r < 0 ? 0 : (r >= H ? H - 1 : r);
-        return rc[(rr % kRing) * ringw];
+        return rc[((rr + kPLag) % kRing) * ringw];
       };
-      // rows [tc0-12, tc0+15] are common to the 4 windows
-      float core = ld(tc0 - 12);
+      if (consecutive) {
+        float core = ld(c0 - 12);
 #pragma unroll 9
-      for (int r = tc0 - 11; r <= tc0 + 15; ++r) core = fmx(core, ld(r));
-      const float u15 = ld(tc0 - 15), u14 = ld(tc0 - 14), u13 = ld(tc0 - 13);
-      const float d16 = ld(tc0 + 16), d17 = ld(tc0 + 17), d18 = ld(tc0 + 18);
-      o0 = fmx(core, fmx3(u15, u14, u13));
-      o1 = fmx3(core, fmx(u14, u13), d16);
-      o2 = fmx3(core, u13, fmx(d16, d17));
-      o3 = fmx(core, fmx3(d16, d17, d18));
+        for (int r = c0 - 11; r <= c0 + 15; ++r) core = fmx(core, ld(r));
+        const float u15 = ld(c0 - 15), u14 = ld(c0 - 14), u13 = ld(c0 - 13);
+        const float d16 = ld(c0 + 16), d17 = ld(c0 + 17), d18 = ld(c0 + 18);
+        o[0] = fmx(core, fmx3(u15, u14, u13));
+        o[1] = fmx3(core, fmx(u14, u13), d16);
+        o[2] = fmx3(core, u13, fmx(d16, d17));
+        o[3] = fmx(core, fmx3(d16, d17, d18));
+      } else {  // frame ends: each row centre clamped separately
+#pragma unroll
+        for (int j = 0; j < kB; ++j) {
+          const int cj = min(max(c0 + j, 0), H - 1);
+          float m = ld(cj - kLF);
+#pragma unroll 5
+          for (int r = cj - kLF + 1; r <= cj + kLF; ++r) m = fmx(m, ld(r));
+          o[j] = m;
+        }
+      }
     }
-    V[0 * kVC + sc] = o0;
-    V[1 * kVC + sc] = o1;
-    V[2 * kVC + sc] = o2;
-    V[3 * kVC + sc] = o3;
+#pragma unroll
+    for (int j = 0; j < kB; ++j) V[j * kVC + sc] = o[j];
   }
   __syncwarp();
 }
 
-// max over scratch row j, columns [4*lane + c, 4*lane + c + 30]  (<-> x-15 .. x+15)
-__device__ __forceinline__ float large_fill_pixel(const float* __restrict__ V, int j, int lane, int c) {
+// step B: max over scratch row j, columns [4*lane + c, 4*lane + c + 30]  (<-> x-15 .. x+15)
+__device__ __forceinline__ float lf_pixel(const float* __restrict__ V, int j, int lane, int c) {
   const float* vr = V + j * kVC + 4 * lane + c;
   float m = vr[0];
 #pragma unroll 10
   for (int d = 1; d <= 2 * kLF; ++d) m = fmx(m, vr[d]);
   return m;
+}
+
+// ---------------------------------------------------------------------------
+// per-item state and one 4-row iteration (EDGE: rows may leave the frame)
+// ---------------------------------------------------------------------------
+struct State {
+  const float* src;
+  float* dst;
+  const float* rring;  // consumer read base: ring + clamped lane column
+  float* wring;        // producer write base: ring + lane column (owned lanes only)
+  float* ring;
+  float* V;
+  int ringw, x0, lane, L, p0, p1;
+  unsigned own, outm, oob, oobL, oobR;
+  bool woob;
+  float nb[4];  // -FMAX where the consumer needs the column, +FMAX elsewhere
+  int T0[4];
+  float top[4];
+  int tmin, tmax;
+  bool skip;
+  F4 c1[2], c2[2], c3[4], c4[4], c5[6], gc[4], mprev[2], nx[kB];
+  unsigned umax;
+  bool had_empty, still_empty;
+  int srcL, srcR, compR;  // replicate sources for out-of-frame columns
+};
+
+template <int VEC, bool FULL, int BLUR, bool EDGE>
+__device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
+  const int H = p.H, W = p.W;
+  const int t0 = kB * k;
+  const int tp = t0 - kPLag;
+  // ======================= producer =======================
+  if (FULL && !S.skip && tp > S.tmax) S.skip = true;
+  F4 f[kB];
+  if (!S.skip) {
+    F4 a[kB];
+#pragma unroll
+    for (int j = 0; j < kB; ++j) {
+      a[j] = S.nx[j];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float v = a[j].v[c];
+        S.umax = max(S.umax, __float_as_uint(v));
+        a[j].v[c] = v > kValid ? p.md - v : 0.0f;
+      }
+    }
+    // prefetch the next block; stops once its stage-5 rows lie above every r0
+    const bool next_needed = !FULL || (t0 + kB - kPLag <= S.tmax);
+#pragma unroll
+    for (int j = 0; j < kB; ++j) {
+      const int t = t0 + kB + j;
+      if ((!EDGE || t < H) && next_needed)
+        S.nx[j] = load4<VEC, true>(S.src + (int64_t)(H - 1 - t) * W, S.x0, W);
+      else
+        set_row(S.nx[j], 0.f);
+    }
+    // --- cross3 #1 (rows t0-1+j) ---
+    F4 d1[kB];
+    {
+      const F4 in[kB + 2] = {S.c1[0], S.c1[1], a[0], a[1], a[2], a[3]};
+#pragma unroll
+      for (int j = 0; j < kB; ++j) {
+        const Ext<1> e = ext_row<1>(in[j + 1]);
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          d1[j].v[c] = fmx3(fmx3(in[j].v[c], in[j + 1].v[c], in[j + 2].v[c]), e.e[c], e.e[c + 2]);
+      }
+      S.c1[0] = a[2], S.c1[1] = a[3];
+#pragma unroll
+      for (int j = 0; j < kB; ++j) {
+        if (EDGE && (t0 - 1 + j < 0 || t0 - 1 + j >= H)) set_row(d1[j], 0.f);
+        if (S.woob) fix_oob(d1[j], S.oob, 0.f);
+      }
+    }
+    // --- cross3 #2 (rows t0-2+j) ---
+    F4 d2[kB];
+    {
+      const F4 in[kB + 2] = {S.c2[0], S.c2[1], d1[0], d1[1], d1[2], d1[3]};
+#pragma unroll
+      for (int j = 0; j < kB; ++j) {
+        const Ext<1> e = ext_row<1>(in[j + 1]);
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          d2[j].v[c] = fmx3(fmx3(in[j].v[c], in[j + 1].v[c], in[j + 2].v[c]), e.e[c], e.e[c + 2]);
+      }
+      S.c2[0] = d1[2], S.c2[1] = d1[3];
+#pragma unroll
+      for (int j = 0; j < kB; ++j) {
+        if (EDGE && (t0 - 2 + j < 0 || t0 - 2 + j >= H)) set_row(d2[j], 0.f);
+        if (S.woob) fix_oob(d2[j], S.oob, 0.f);
+      }
+    }
+    // --- close: max5 (rows t0-4+j) ---
+    F4 m5[kB];
+    {
+      const F4 in[kB + 4] = {S.c3[0], S.c3[1], S.c3[2], S.c3[3], d2[0], d2[1], d2[2], d2[3]};
+      F4 vv[kB];
+      vwin2<OpMax>(in, vv);
+#pragma unroll
+      for (int j = 0; j < kB; ++j) m5[j] = hwin2<OpMax>(ext_row<2>(vv[j]));
+#pragma unroll
+      for (int i = 0; i < 4; ++i) S.c3[i] = d2[i];
+#pragma unroll
+      for (int j = 0; j < kB; ++j) {
+        if (EDGE && (t0 - 4 + j < 0 || t0 - 4 + j >= H)) set_row(m5[j], kFMax);
+        if (S.woob) fix_oob(m5[j], S.oob, kFMax);
+      }
+    }
+    // --- close: min5 (rows t0-6+j) ---
+    F4 cl[kB];
+    {
+      const F4 in[kB + 4] = {S.c4[0], S.c4[1], S.c4[2], S.c4[3], m5[0], m5[1], m5[2], m5[3]};
+      F4 vv[kB];
+      vwin2<OpMin>(in, vv);
+#pragma unroll
+      for (int j = 0; j < kB; ++j) cl[j] = hwin2<OpMin>(ext_row<2>(vv[j]));
+#pragma unroll
+      for (int i = 0; i < 4; ++i) S.c4[i] = m5[i];
+#pragma unroll
+      for (int j = 0; j < kB; ++j) {
+        if (EDGE && (t0 - 6 + j < 0 || t0 - 6 + j >= H)) set_row(cl[j], 0.f);
+        if (S.woob) fix_oob(cl[j], S.oob, 0.f);
+      }
+    }
+    // --- small fill: masked max7 (rows t0-9+j) ---
+    {
+      const F4 in[kB + 6] = {S.c5[0], S.c5[1], S.c5[2], S.c5[3], S.c5[4], S.c5[5], cl[0], cl[1], cl[2], cl[3]};
+      F4 vv[kB];
+      vwin3<OpMax>(in, vv);
+#pragma unroll
+      for (int j = 0; j < kB; ++j) {
+        const F4 h7 = hwin3<OpMax>(ext_row<3>(vv[j]));
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const float ctr = in[j + 3].v[c];
+          f[j].v[c] = ctr > kValid ? ctr : h7.v[c];
+        }
+      }
+      S.c5[0] = S.c5[4], S.c5[1] = S.c5[5];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) S.c5[i + 2] = cl[i];
+    }
+    // --- extend to top (FULL; only blocks reaching some column's r0) ---
+    if (FULL && tp + kB - 1 >= S.tmin) {
+#pragma unroll
+      for (int j = 0; j < kB; ++j) {
+        const int t = tp + j;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (t == S.T0[c]) S.top[c] = f[j].v[c];
+          if (t > S.T0[c]) f[j].v[c] = S.top[c];
+        }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < kB; ++j)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) f[j].v[c] = S.top[c];
+  }
+  // --- ring store: ring slot of row t is (t + 9) mod 40, so this block is slots 4*(k mod 10) + j ---
+  if (S.own) {
+    float* w = S.wring + (k % kRingBlocks) * kB * S.ringw;
+#pragma unroll
+    for (int j = 0; j < kB; ++j)
+      if (!EDGE || (tp + j >= 0 && tp + j < H))
+        *reinterpret_cast<float4*>(w + j * S.ringw) = make_float4(f[j].v[0], f[j].v[1], f[j].v[2], f[j].v[3]);
+  }
+  __syncthreads();
+  // ======================= consumer =======================
+  const int tc0 = t0 - kCLag;
+  if (k < kKFirst) return;
+  F4 v6[kB];
+  {
+    // rows tc0 + j live in slots 4*((k + 6) mod 10) + j when inside the frame
+    const float* r = S.rring + ((k + kRingBlocks - kLag / kB) % kRingBlocks) * kB * S.ringw;
+#pragma unroll
+    for (int j = 0; j < kB; ++j) {
+      const float* rr = r + j * S.ringw;
+      if (EDGE) {
+        const int t = min(max(tc0 + j, 0), H - 1);
+        rr = S.rring + ((t + kPLag) % kRing) * S.ringw;
+      }
+      const float4 q = *reinterpret_cast<const float4*>(rr);
+      v6[j].v[0] = q.x, v6[j].v[1] = q.y, v6[j].v[2] = q.z, v6[j].v[3] = q.w;
+    }
+  }
+  if (FULL) {
+    // any needed empty pixel in this block? (max with nb masks unneeded columns)
+    float mn = kFMax;
+#pragma unroll
+    for (int j = 0; j < kB; ++j)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) mn = fminf(mn, fmaxf(v6[j].v[c], S.nb[c]));
+    const bool e = !(mn > kValid);
+    if (__any_sync(kFull, e)) {
+      S.had_empty |= e;
+      lf_vstep(S.ring, S.ringw, S.p0, S.p1, H, S.L, S.lane, tc0, !EDGE || (tc0 >= 0 && tc0 + kB - 1 < H), S.V);
+#pragma unroll
+      for (int j = 0; j < kB; ++j)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (!(fmaxf(v6[j].v[c], S.nb[c]) > kValid)) {
+            v6[j].v[c] = lf_pixel(S.V, j, S.lane, c);
+            S.still_empty |= !(v6[j].v[c] > kValid);
+          }
+      __syncwarp();
+    }
+  }
+  // out-of-frame columns replicate the edge column (the blur needs true replicate)
+  if (S.woob) {
+#pragma unroll
+    for (int j = 0; j < kB; ++j) {
+      const float eL = __shfl_sync(kFull, v6[j].v[0], S.srcL);
+      const float sr = S.compR == 0 ? v6[j].v[0] : (S.compR == 1 ? v6[j].v[1] : (S.compR == 2 ? v6[j].v[2] : v6[j].v[3]));
+      const float eR = __shfl_sync(kFull, sr, S.srcR);
+      fix_oob(v6[j], S.oobL, eL);
+      fix_oob(v6[j], S.oobR, eR);
+    }
+  }
+  if constexpr (BLUR == DFC_BLUR_GAUSSIAN) {
+    F4 h[kB];
+#pragma unroll
+    for (int j = 0; j < kB; ++j) {
+      const Ext<2> e = ext_row<2>(v6[j]);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float a = p.gw[0] * e.e[c];
+        a = fmaf(p.gw[1], e.e[c + 1], a);
+        a = fmaf(p.gw[2], e.e[c + 2], a);
+        a = fmaf(p.gw[3], e.e[c + 3], a);
+        h[j].v[c] = fmaf(p.gw[4], e.e[c + 4], a);
+      }
+    }
+    if (EDGE && k == kKFirst) {  // rows above row 0 replicate it (tc0 = -1: h[0] is row 0)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) S.gc[i] = h[0];
+    }
+    const F4 in[kB + 4] = {S.gc[0], S.gc[1], S.gc[2], S.gc[3], h[0], h[1], h[2], h[3]};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) S.gc[i] = h[i];
+    F4 mk[kB];
+    if (!FULL) {  // pre-blur validity of output rows tc0-2+j (pipeline.py:212-214)
+      mk[0] = S.mprev[0], mk[1] = S.mprev[1], mk[2] = v6[0], mk[3] = v6[1];
+      S.mprev[0] = v6[2], S.mprev[1] = v6[3];
+    }
+#pragma unroll
+    for (int j = 0; j < kB; ++j) {
+      const int t = tc0 + j - 2;  // output row (processing order)
+      if (EDGE && (t < 0 || t >= H)) continue;
+      F4 o;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float a = p.gw[0] * in[j].v[c];
+        a = fmaf(p.gw[1], in[j + 1].v[c], a);
+        a = fmaf(p.gw[2], in[j + 2].v[c], a);
+        a = fmaf(p.gw[3], in[j + 3].v[c], a);
+        a = fmaf(p.gw[4], in[j + 4].v[c], a);
+        o.v[c] = a > kValid ? p.md - a : 0.0f;
+        if (!FULL && !(mk[j].v[c] > kValid)) o.v[c] = 0.0f;
+      }
+      if (S.outm) store4<VEC>(S.dst + (int64_t)(H - 1 - t) * W, S.x0, o, S.outm);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < kB; ++j) {
+      const int t = tc0 + j;
+      if (EDGE && (t < 0 || t >= H)) continue;
+      F4 o;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) o.v[c] = v6[j].v[c] > kValid ? p.md - v6[j].v[c] : 0.0f;
+      if (S.outm) store4<VEC>(S.dst + (int64_t)(H - 1 - t) * W, S.x0, o, S.outm);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -448,375 +726,105 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
     __syncthreads();
     if (item >= total) break;
     const int64_t frame = item / p.strips;
-    const int strip = (int)(item % p.strips);
-    int o0, o1, p0, p1;
-    WarpGeo g;
-    item_geometry(strip, p, warp, o0, o1, p0, p1, g);
-    const int ringw = ((p1 - p0) + 3) & ~3;
-    float* ring = smem;
-    float* V = smem + kRing * ringw + warp * (kB * kVC);
-    const bool active = warp < g.nw;
-    const float* src = p.in + frame * HW;
-    float* dst = p.out + frame * HW;
-    const int x0 = g.L + 4 * lane;
-
-    // per-lane column masks
-    unsigned incol = 0, oob = 0, own = 0, need = 0, outm = 0;
+    Geo g;
+    item_geometry((int)(item % p.strips), p, warp, g);
+    State S;
+    S.ringw = ((g.p1 - g.p0) + 3) & ~3;
+    S.ring = smem;
+    S.V = smem + kRing * S.ringw + warp * (kB * kVC);
+    S.src = p.in + frame * HW;
+    S.dst = p.out + frame * HW;
+    S.x0 = g.L + 4 * lane;
+    S.lane = lane;
+    S.L = g.L;
+    S.p0 = g.p0;
+    S.p1 = g.p1;
+    S.wring = S.ring + (S.x0 - g.p0);
+    S.rring = S.ring + (min(max(S.x0, g.p0), g.p0 + S.ringw - 4) - g.p0);
+    unsigned incol = 0;
+    S.own = S.outm = S.oob = S.oobL = S.oobR = 0;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      const int x = x0 + c;
-      incol |= (unsigned)(x < W) << c;
-      oob |= (unsigned)(x >= W) << c;
-      own |= (unsigned)(x >= g.q0 && x < g.q1) << c;
-      need |= (unsigned)(x >= max(max(g.q0 - 2, o0 - 2), p0) && x < min(min(g.q1 + 2, o1 + 2), p1) && x < W) << c;
-      outm |= (unsigned)(x >= max(g.q0, o0) && x < min(g.q1, o1)) << c;
+      const int x = S.x0 + c;
+      incol |= (unsigned)(x >= 0 && x < W) << c;
+      S.oobL |= (unsigned)(x < 0) << c;
+      S.oobR |= (unsigned)(x >= W) << c;
+      S.own |= (unsigned)(x >= g.q0 && x < g.q1) << c;
+      S.outm |= (unsigned)(x >= max(g.q0, g.o0) && x < min(g.q1, g.o1)) << c;
+      const bool need = x >= max(max(g.q0 - 2, g.o0 - 2), max(g.p0, 0)) && x < min(min(g.q1 + 2, g.o1 + 2), g.p1);
+      S.nb[c] = need ? -kFMax : kFMax;
     }
-    const bool woob = __any_sync(kFull, oob != 0);
-    unsigned umax = 0;
+    S.oob = S.oobL | S.oobR;
+    S.woob = __any_sync(kFull, S.oob != 0);
+    S.srcL = (0 - g.L) >> 2;  // lane holding column 0 (component 0)
+    S.srcR = (W - 1 - g.L) >> 2;
+    S.compR = (W - 1 - g.L) & 3;
+    S.srcL = min(max(S.srcL, 0), 31);
+    S.srcR = min(max(S.srcR, 0), 31);
+    S.umax = 0;
+    S.had_empty = S.still_empty = false;
+    S.skip = false;
 
-    // ---------------- phase 1: r0 per column ---------------------------
-    int T0[4] = {INT_MAX, INT_MAX, INT_MAX, INT_MAX};
-    int tmax = INT_MAX, tmin = INT_MAX;
-    if (FULL && active) {
-      phase1<VEC>(src, p, x0, lane, own != 0, incol, T0, umax);
+    // ---------------- phase 1 ----------------
+#pragma unroll
+    for (int c = 0; c < 4; ++c) S.T0[c] = INT_MAX, S.top[c] = 0.f;
+    S.tmax = S.tmin = INT_MAX;
+    if (FULL) {
+      phase1<VEC>(S.src, p, S.x0, S.own != 0, incol, S.T0, S.umax);
       int mx = INT_MIN, mn = INT_MAX;
 #pragma unroll
       for (int c = 0; c < 4; ++c)
-        if (own >> c & 1) {
-          mx = max(mx, T0[c]);
-          mn = min(mn, T0[c]);
+        if (S.own >> c & 1) {
+          mx = max(mx, S.T0[c]);
+          mn = min(mn, S.T0[c]);
         }
-      tmax = __reduce_max_sync(kFull, mx);
-      tmin = __reduce_min_sync(kFull, mn);
+      S.tmax = __reduce_max_sync(kFull, mx);
+      S.tmin = __reduce_min_sync(kFull, mn);
     }
 
-    // ---------------- phase 2: bottom-up streaming -------------------------
-    F4 c1[2], c2[2], c3[4], c4[4], c5[6], gc[4];
+    // ---------------- phase 2 ----------------
 #pragma unroll
-    for (int i = 0; i < 2; ++i) set_row(c1[i], 0.f), set_row(c2[i], 0.f);
+    for (int i = 0; i < 2; ++i) set_row(S.c1[i], 0.f), set_row(S.c2[i], 0.f), set_row(S.mprev[i], 0.f);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) set_row(c3[i], 0.f), set_row(c4[i], kFMax), set_row(gc[i], 0.f);
+    for (int i = 0; i < 4; ++i) set_row(S.c3[i], 0.f), set_row(S.c4[i], kFMax), set_row(S.gc[i], 0.f);
 #pragma unroll
-    for (int i = 0; i < 6; ++i) set_row(c5[i], 0.f);
-    float top[4] = {0.f, 0.f, 0.f, 0.f};
-    F4 hlast;
-    set_row(hlast, 0.f);
-    bool had_empty = false, still_empty = false;
+    for (int i = 0; i < 6; ++i) set_row(S.c5[i], 0.f);
+#pragma unroll
+    for (int j = 0; j < kB; ++j)
+      S.nx[j] = j < H ? load4<VEC, true>(S.src + (int64_t)(H - 1 - j) * W, S.x0, W) : F4{{0.f, 0.f, 0.f, 0.f}};
 
-    // prefetch of the first input block (rows t = 0..3 <-> y = H-1..H-4)
-    F4 nx[kB];
-#pragma unroll
-    for (int j = 0; j < kB; ++j) {
-      set_row(nx[j], 0.f);
-      if (active && j < H) nx[j] = load4<VEC>(src + (int64_t)(H - 1 - j) * W, x0, W);
-    }
+    // iterations with every row inside the frame run the lean body
+    const int K = (H + kCLag + 2) / kB + 1;
+    const int kLo = (kCLag + 2 + kB - 1) / kB;  // tc0 - 2 >= 0 and tp >= 0
+    const int kHi = (H - 2 * kB) / kB;           // t0 + 7 <= H - 1 and tc0 + 3 <= H - 1
+    int k = 0;
+    for (; k < min(kLo, K); ++k) iterate<VEC, FULL, BLUR, true>(p, S, k);
+    for (; k <= kHi; ++k) iterate<VEC, FULL, BLUR, false>(p, S, k);
+    for (; k < K; ++k) iterate<VEC, FULL, BLUR, true>(p, S, k);
 
-    const int K = (H + kCLag + 2 + kB) / kB + 1;
-    bool skip = false;
-    for (int k = 0; k < K; ++k) {
-      const int t0 = kB * k;
-      // ======================= producer =======================
-      if (active) {
-        const int tp = t0 - kPLag;  // first stage-5 row of this block
-        if (FULL && !skip && tp > tmax) skip = true;
-        F4 f[kB];
-        if (!skip) {
-          F4 a[kB];
-#pragma unroll
-          for (int j = 0; j < kB; ++j) {
-            a[j] = nx[j];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              const float v = a[j].v[c];
-              if (t0 + j < H) umax = max(umax, (incol >> c & 1) ? __float_as_uint(v) : 0u);
-              a[j].v[c] = v > kValid ? p.md - v : 0.0f;
-            }
-          }
-          // prefetch the next block (skipped once its stage-5 rows are above every r0)
-          const bool next_needed = !FULL || (t0 + kB - kPLag <= tmax);
-#pragma unroll
-          for (int j = 0; j < kB; ++j) {
-            const int t = t0 + kB + j;
-            set_row(nx[j], 0.f);
-            if (next_needed && t < H) nx[j] = load4<VEC>(src + (int64_t)(H - 1 - t) * W, x0, W);
-          }
-          // --- cross3 #1 (rows t0-1+j) ---
-          F4 d1[kB];
-          {
-            F4 in[kB + 2] = {c1[0], c1[1], a[0], a[1], a[2], a[3]};
-#pragma unroll
-            for (int j = 0; j < kB; ++j) {
-              const Ext<1> e = ext_row<1>(in[j + 1], lane);
-#pragma unroll
-              for (int c = 0; c < 4; ++c)
-                d1[j].v[c] = fmx3(fmx3(in[j].v[c], in[j + 1].v[c], in[j + 2].v[c]), e.e[c], e.e[c + 2]);
-            }
-            c1[0] = a[2], c1[1] = a[3];
-#pragma unroll
-            for (int j = 0; j < kB; ++j) {
-              const int t = t0 - 1 + j;
-              if (t < 0 || t >= H) set_row(d1[j], 0.f);
-              if (woob) fix_oob(d1[j], oob, 0.f);
-            }
-          }
-          // --- cross3 #2 (rows t0-2+j) ---
-          F4 d2[kB];
-          {
-            F4 in[kB + 2] = {c2[0], c2[1], d1[0], d1[1], d1[2], d1[3]};
-#pragma unroll
-            for (int j = 0; j < kB; ++j) {
-              const Ext<1> e = ext_row<1>(in[j + 1], lane);
-#pragma unroll
-              for (int c = 0; c < 4; ++c)
-                d2[j].v[c] = fmx3(fmx3(in[j].v[c], in[j + 1].v[c], in[j + 2].v[c]), e.e[c], e.e[c + 2]);
-            }
-            c2[0] = d1[2], c2[1] = d1[3];
-#pragma unroll
-            for (int j = 0; j < kB; ++j) {
-              const int t = t0 - 2 + j;
-              if (t < 0 || t >= H) set_row(d2[j], 0.f);
-              if (woob) fix_oob(d2[j], oob, 0.f);
-            }
-          }
-          // --- close: max5 (rows t0-4+j) ---
-          F4 m5[kB];
-          {
-            F4 in[kB + 4] = {c3[0], c3[1], c3[2], c3[3], d2[0], d2[1], d2[2], d2[3]};
-            F4 vv[kB];
-            vwin2<OpMax>(in, vv);
-#pragma unroll
-            for (int j = 0; j < kB; ++j) m5[j] = hwin2<OpMax>(ext_row<2>(vv[j], lane));
-#pragma unroll
-            for (int i = 0; i < 4; ++i) c3[i] = d2[i];
-#pragma unroll
-            for (int j = 0; j < kB; ++j) {
-              const int t = t0 - 4 + j;
-              if (t < 0 || t >= H) set_row(m5[j], kFMax);
-              if (woob) fix_oob(m5[j], oob, kFMax);
-            }
-          }
-          // --- close: min5 (rows t0-6+j) ---
-          F4 cl[kB];
-          {
-            F4 in[kB + 4] = {c4[0], c4[1], c4[2], c4[3], m5[0], m5[1], m5[2], m5[3]};
-            F4 vv[kB];
-            vwin2<OpMin>(in, vv);
-#pragma unroll
-            for (int j = 0; j < kB; ++j) cl[j] = hwin2<OpMin>(ext_row<2>(vv[j], lane));
-#pragma unroll
-            for (int i = 0; i < 4; ++i) c4[i] = m5[i];
-#pragma unroll
-            for (int j = 0; j < kB; ++j) {
-              const int t = t0 - 6 + j;
-              if (t < 0 || t >= H) set_row(cl[j], 0.f);
-              if (woob) fix_oob(cl[j], oob, 0.f);
-            }
-          }
-          // --- small fill: masked max7 (rows t0-9+j) ---
-          {
-            F4 in[kB + 6] = {c5[0], c5[1], c5[2], c5[3], c5[4], c5[5], cl[0], cl[1], cl[2], cl[3]};
-            F4 vv[kB];
-            vwin3<OpMax>(in, vv);
-#pragma unroll
-            for (int j = 0; j < kB; ++j) {
-              const F4 h7 = hwin3<OpMax>(ext_row<3>(vv[j], lane));
-#pragma unroll
-              for (int c = 0; c < 4; ++c) {
-                const float ctr = in[j + 3].v[c];
-                f[j].v[c] = ctr > kValid ? ctr : h7.v[c];
-              }
-            }
-#pragma unroll
-            for (int i = 0; i < 2; ++i) c5[i] = c5[i + 4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) c5[i + 2] = cl[i];
-          }
-          // --- extend to top (FULL) ---
-          if (FULL && tp + kB - 1 >= tmin) {
-#pragma unroll
-            for (int j = 0; j < kB; ++j) {
-              const int t = tp + j;
-#pragma unroll
-              for (int c = 0; c < 4; ++c) {
-                if (t == T0[c]) top[c] = f[j].v[c];
-                if (t > T0[c]) f[j].v[c] = top[c];
-              }
-            }
-          }
-        } else {
-          // every owned column is above its r0: stage 5 is the captured top value
-#pragma unroll
-          for (int j = 0; j < kB; ++j)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) f[j].v[c] = top[c];
-        }
-        // --- ring store (owned columns, rows inside the frame) ---
-        if (own) {
-#pragma unroll
-          for (int j = 0; j < kB; ++j) {
-            const int t = tp + j;
-            if (t >= 0 && t < H) {
-              const int slot = (t + kRing * 4) % kRing;
-              *reinterpret_cast<float4*>(ring + slot * ringw + (x0 - p0)) =
-                  make_float4(f[j].v[0], f[j].v[1], f[j].v[2], f[j].v[3]);
-            }
-          }
-        }
-      }
-      __syncthreads();
-      // ======================= consumer =======================
-      const int tc0 = t0 - kCLag;  // consumer rows tc0 .. tc0+3
-      if (active && tc0 + kB - 1 >= 0) {
-        F4 v6[kB];
-        unsigned em[kB];
-        bool any_empty = false;
-        const int xr = min(max(x0, p0), ((p1 - p0 + 3) & ~3) + p0 - 4);  // clamp lane read into the ring row
-#pragma unroll
-        for (int j = 0; j < kB; ++j) {
-          const int t = tc0 + j;
-          em[j] = 0;
-          if (t >= 0 && t < H) {
-            const float4 q = *reinterpret_cast<const float4*>(ring + (t % kRing) * ringw + (xr - p0));
-            v6[j].v[0] = q.x, v6[j].v[1] = q.y, v6[j].v[2] = q.z, v6[j].v[3] = q.w;
-            if (FULL) {
-#pragma unroll
-              for (int c = 0; c < 4; ++c) em[j] |= (unsigned)((need >> c & 1) && !(v6[j].v[c] > kValid)) << c;
-              any_empty |= em[j] != 0;
-            }
-          } else {
-            set_row(v6[j], 0.f);
-          }
-        }
-        if (FULL) {
-          had_empty |= any_empty;
-          if (__any_sync(kFull, any_empty)) {
-            large_fill_vstep(ring, ringw, p0, p1, H, g.L, lane, tc0, V);
-#pragma unroll
-            for (int j = 0; j < kB; ++j)
-#pragma unroll
-              for (int c = 0; c < 4; ++c)
-                if (em[j] >> c & 1) v6[j].v[c] = large_fill_pixel(V, j, lane, c);
-            __syncwarp();
-          }
-#pragma unroll
-          for (int j = 0; j < kB; ++j)
-            if (em[j]) {
-#pragma unroll
-              for (int c = 0; c < 4; ++c)
-                if ((em[j] >> c & 1) && !(v6[j].v[c] > kValid)) still_empty = true;
-            }
-        }
-        // right frame edge: columns >= W replicate column W-1 (Gaussian needs true replicate)
-        if (woob) {
-          const int xe = W - 1 - g.L;  // warp-relative column of W-1
-#pragma unroll
-          for (int j = 0; j < kB; ++j) {
-            const float e0 = __shfl_sync(kFull, v6[j].v[0], xe >> 2);
-            const float e1 = __shfl_sync(kFull, v6[j].v[1], xe >> 2);
-            const float e2 = __shfl_sync(kFull, v6[j].v[2], xe >> 2);
-            const float e3 = __shfl_sync(kFull, v6[j].v[3], xe >> 2);
-            const int cc = xe & 3;
-            const float e = cc == 0 ? e0 : (cc == 1 ? e1 : (cc == 2 ? e2 : e3));
-            fix_oob(v6[j], oob, e);
-          }
-        }
-        if constexpr (BLUR == DFC_BLUR_GAUSSIAN) {
-          F4 h[kB];
-#pragma unroll
-          for (int j = 0; j < kB; ++j) {
-            const Ext<2> e = ext_row<2>(v6[j], lane);
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              float a = p.gw[0] * e.e[c];
-              a = fmaf(p.gw[1], e.e[c + 1], a);
-              a = fmaf(p.gw[2], e.e[c + 2], a);
-              a = fmaf(p.gw[3], e.e[c + 3], a);
-              h[j].v[c] = fmaf(p.gw[4], e.e[c + 4], a);
-            }
-          }
-          // vertical replicate at the frame ends
-#pragma unroll
-          for (int j = 0; j < kB; ++j) {
-            if (tc0 + j >= H) h[j] = hlast;
-            else if (tc0 + j >= 0) hlast = h[j];
-          }
-          if (tc0 <= 0 && tc0 + kB - 1 >= 0) {  // block holding row 0: rows above it replicate row 0
-            const int j0 = -tc0;
-            F4 h0 = h[0];
-#pragma unroll
-            for (int j = 1; j < kB; ++j)
-              if (j == j0) h0 = h[j];
-#pragma unroll
-            for (int j = 0; j < kB; ++j)
-              if (j < j0) h[j] = h0;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) gc[i] = h0;
-          }
-          F4 in[kB + 4] = {gc[0], gc[1], gc[2], gc[3], h[0], h[1], h[2], h[3]};
-#pragma unroll
-          for (int i = 0; i < 4; ++i) gc[i] = h[i];
-#pragma unroll
-          for (int j = 0; j < kB; ++j) {
-            const int t = tc0 + j - 2;  // output row (processing order)
-            if (t < 0 || t >= H) continue;
-            F4 o;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              float a = p.gw[0] * in[j].v[c];
-              a = fmaf(p.gw[1], in[j + 1].v[c], a);
-              a = fmaf(p.gw[2], in[j + 2].v[c], a);
-              a = fmaf(p.gw[3], in[j + 3].v[c], a);
-              a = fmaf(p.gw[4], in[j + 4].v[c], a);
-              o.v[c] = a > kValid ? p.md - a : 0.0f;
-            }
-            if (!FULL) {  // partial: re-impose the pre-blur validity (pipeline.py:212-214)
-              const float4 q = *reinterpret_cast<const float4*>(ring + (t % kRing) * ringw + (xr - p0));
-              const float m[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-              for (int c = 0; c < 4; ++c)
-                if (!(m[c] > kValid)) o.v[c] = 0.0f;
-            }
-            if (outm) store4<VEC>(dst + (int64_t)(H - 1 - t) * W, x0, o, outm);
-          }
-        } else {  // BLUR_NONE: invert back directly
-#pragma unroll
-          for (int j = 0; j < kB; ++j) {
-            const int t = tc0 + j;
-            if (t < 0 || t >= H) continue;
-            F4 o;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) o.v[c] = v6[j].v[c] > kValid ? p.md - v6[j].v[c] : 0.0f;
-            if (outm) store4<VEC>(dst + (int64_t)(H - 1 - t) * W, x0, o, outm);
-          }
-        }
-      }
-    }
     // ---------------- per-frame flags ----------------
-    if (active) {
-      const unsigned um = __reduce_max_sync(kFull, umax);
-      const bool he = __any_sync(kFull, had_empty);
-      const bool se = __any_sync(kFull, still_empty);
-      if (lane == 0) {
-        atomicMax(p.umax + frame, um);
-        if (FULL && he && p.iters) atomicOr(p.iters + frame, 1);
-        if (FULL && se) {
-          atomicOr(p.status + frame, kNeedsStaged);
-          atomicAdd(p.nfallback, 1ull);
-        }
+    const unsigned um = __reduce_max_sync(kFull, S.umax);
+    const bool he = __any_sync(kFull, S.had_empty);
+    const bool se = __any_sync(kFull, S.still_empty);
+    if (lane == 0) {
+      atomicMax(p.umax + frame, um);
+      if (FULL && he && p.iters) atomicOr(p.iters + frame, 1);
+      if (FULL && se) {
+        atomicOr(p.status + frame, kNeedsStaged);
+        atomicAdd(p.nfallback, 1ull);
       }
     }
     __syncthreads();  // ring reuse by the next item
   }
 }
 
-// Per-frame status from the input's max bit pattern; rescans frames whose
-// max is suspicious (negative, non-finite or >= max_depth) to classify.
+// Per-frame status from the input's largest bit pattern; frames whose max is
+// suspicious (negative sign, non-finite, >= max_depth) are rescanned.
 __global__ void finalize_kernel(const float* __restrict__ in, int64_t HW, const unsigned* __restrict__ umax,
                                 uint32_t* status, float md) {
   const int64_t b = blockIdx.x;
   const unsigned u = umax[b];
-  const unsigned mdb = __float_as_uint(md);
-  if (u < mdb) {
+  if (u < __float_as_uint(md)) {
     if (u <= __float_as_uint(kValid) && threadIdx.x == 0) atomicOr(status + b, DFC_ST_DEGENERATE);
     return;
   }
@@ -825,9 +833,12 @@ __global__ void finalize_kernel(const float* __restrict__ in, int64_t HW, const 
   bool anyv = false;
   for (int64_t i = threadIdx.x; i < HW; i += blockDim.x) {
     const float v = src[i];
-    if (!isfinite(v)) bits |= DFC_ST_NONFINITE;
-    else if (v < 0.0f) bits |= DFC_ST_NEGATIVE;
-    else if (v >= md) bits |= DFC_ST_RANGE;
+    if (!isfinite(v))
+      bits |= DFC_ST_NONFINITE;
+    else if (v < 0.0f)
+      bits |= DFC_ST_NEGATIVE;
+    else if (v >= md)
+      bits |= DFC_ST_RANGE;
     anyv |= v > kValid;
   }
   bits = __reduce_or_sync(kFull, bits);
@@ -848,9 +859,22 @@ __global__ void finalize_kernel(const float* __restrict__ in, int64_t HW, const 
 }
 
 struct Layout {
-  int strips, SW;
+  int strips, SW, nw;
   size_t smem;
 };
+
+int host_warps(int o0, int o1, int W) {
+  const int p0 = o0 == 0 ? 0 : std::max(0, (o0 - 17) & ~3);
+  const int p1 = o1 == W ? W : std::min(W, (o1 + 17 + 3) & ~3);
+  int q0 = p0, nw = 0;
+  while (q0 < p1) {
+    const int L = q0 == 0 ? -4 : q0 - kHalo;
+    const int q1 = (p1 == W && L + kLW - 4 >= W) ? W : std::min(p1, L + kLW - kHalo);
+    q0 = q1;
+    ++nw;
+  }
+  return nw;
+}
 
 Layout layout(int W) {
   Layout L;
@@ -862,9 +886,17 @@ Layout layout(int W) {
     L.SW = (((W + L.strips - 1) / L.strips) + 3) & ~3;
     L.strips = (W + L.SW - 1) / L.SW;
   }
-  const int pw = L.strips == 1 ? W : L.SW + 2 * 20;
-  const int ringw = (pw + 3) & ~3;
-  L.smem = (size_t)kRing * ringw * 4 + (size_t)kNW * kB * kVC * 4;
+  L.nw = 0;
+  int pwmax = 0;
+  for (int s = 0; s < L.strips; ++s) {
+    const int o0 = s * L.SW, o1 = std::min(W, o0 + L.SW);
+    L.nw = std::max(L.nw, host_warps(o0, o1, W));
+    const int p0 = o0 == 0 ? 0 : std::max(0, (o0 - 17) & ~3);
+    const int p1 = o1 == W ? W : std::min(W, (o1 + 17 + 3) & ~3);
+    pwmax = std::max(pwmax, p1 - p0);
+  }
+  const int ringw = (pwmax + 3) & ~3;
+  L.smem = (size_t)kRing * ringw * 4 + (size_t)L.nw * kB * kVC * 4;
   return L;
 }
 
@@ -874,7 +906,7 @@ cudaError_t launch_t(const Params& p, size_t smem, int grid, cudaStream_t s) {
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   note_launch();
-  k<<<grid, kNW * 32, smem, s>>>(p);
+  k<<<grid, p.nw * 32, smem, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -887,7 +919,8 @@ bool fused_supported(const dfc_config& c, int H, int W) {
   if (c.blur_mode != DFC_BLUR_GAUSSIAN && c.blur_mode != DFC_BLUR_NONE) return false;
   if (c.blur_mode == DFC_BLUR_GAUSSIAN && c.gaussian_size != 5) return false;
   if (H < 16 || W < 16) return false;
-  return layout(W).smem <= 232448;
+  const Layout L = layout(W);
+  return L.nw <= kNW && L.smem <= 232448;
 }
 
 size_t fused_workspace_bytes(const dfc_config&, int64_t B, int, int) {
@@ -907,6 +940,7 @@ cudaError_t launch_fused(const float* in, float* out, int64_t B, int H, int W, c
   const Layout L = layout(W);
   p.strips = L.strips;
   p.SW = L.SW;
+  p.nw = L.nw;
   p.md = c.max_depth;
   {
     const int r = c.gaussian_size / 2;
@@ -931,10 +965,10 @@ cudaError_t launch_fused(const float* in, float* out, int64_t B, int H, int W, c
   const int vec = (W % 4 == 0) ? 4 : ((W % 2 == 0) ? 2 : 1);
   const bool full = c.fill_mode == DFC_FILL_FULL;
   const bool gauss = c.blur_mode == DFC_BLUR_GAUSSIAN;
-#define DFC_DISPATCH(V)                                                                        \
-  (full ? (gauss ? launch_t<V, true, DFC_BLUR_GAUSSIAN>(p, L.smem, grid, s)                    \
-                 : launch_t<V, true, DFC_BLUR_NONE>(p, L.smem, grid, s))                       \
-        : (gauss ? launch_t<V, false, DFC_BLUR_GAUSSIAN>(p, L.smem, grid, s)                   \
+#define DFC_DISPATCH(V)                                                      \
+  (full ? (gauss ? launch_t<V, true, DFC_BLUR_GAUSSIAN>(p, L.smem, grid, s)  \
+                 : launch_t<V, true, DFC_BLUR_NONE>(p, L.smem, grid, s))     \
+        : (gauss ? launch_t<V, false, DFC_BLUR_GAUSSIAN>(p, L.smem, grid, s) \
                  : launch_t<V, false, DFC_BLUR_NONE>(p, L.smem, grid, s)))
   e = vec == 4 ? DFC_DISPATCH(4) : (vec == 2 ? DFC_DISPATCH(2) : DFC_DISPATCH(1));
 #undef DFC_DISPATCH

@@ -278,3 +278,55 @@ def test_cuda_backend_plugin(P):
     w = O.gaussian_weights(5, 1.1)
     assert np.array_equal(be.gaussian_separable(v, w), O.gaussian_separable(v, w))
     assert np.abs(be.bilateral_filter(v, 5, 1.5, 2.0) - O.bilateral_filter(v, 5, 1.5, 2.0)).max() <= 1e-5
+
+
+GEOMS = [(352, 1216), (375, 1242), (40, 130), (16, 16), (17, 203), (100, 1250), (64, 2600), (200, 333), (33, 129)]
+
+
+def _geom_frames(h, w, n, seed):
+    spec = synth.SynthSpec(width=w, height=h, beams=max(4, min(64, h // 3)), density=(0.04, 0.12))
+    return np.stack([synth.make_frame(spec, [900 + seed, i]) for i in range(n)])
+
+
+@pytest.mark.parametrize("h,w", GEOMS)
+@pytest.mark.parametrize("blur,fill", [("gaussian", "full"), ("none", "full"), ("gaussian", "partial"),
+                                       ("none", "partial")])
+def test_fused_geometries_vs_oracle(P, h, w, blur, fill):
+    """Frame shapes that exercise strips, W % 4 != 0, lane halos and tiny H."""
+    frames = _geom_frames(h, w, 3, h * 7 + w)
+    kw = {"blur_mode": blur, "fill_mode": fill}
+    res = P.complete_batch(frames, _pcfg(P, kw))
+    got = res.dense.cpu().numpy()
+    st = res.status.cpu().numpy()
+    for i in range(frames.shape[0]):
+        ref, info = O.complete_with_stats(frames[i], _ocfg(kw))
+        _cmp(got[i], ref, blur)
+        assert int(res.iterations[i]) == info["large_fill_iterations"], (i, st[i])
+
+
+def test_fused_matches_staged_bits_for_selection(P):
+    """Selection-only config: fused and staged paths agree bit for bit."""
+    frames = synth.make_batch(1, 700, 16)
+    kw = {"blur_mode": "none", "fill_mode": "full"}
+    a = P.complete_batch(frames, _pcfg(P, kw)).dense.cpu().numpy()
+    b = P.complete_batch(frames, _pcfg(P, kw), force_staged=True).dense.cpu().numpy()
+    assert np.array_equal(_bits(a), _bits(b))
+
+
+def test_fused_random_sparse_frames(P):
+    """Uniform random sparse points (not scanlines): many empties, columns
+    without points, values near max_depth."""
+    rng = np.random.default_rng(77)
+    frames = np.zeros((6, 120, 300), np.float32)
+    for i in range(6):
+        m = rng.random(frames[i].shape) < [0.002, 0.01, 0.03, 0.08, 0.2, 0.5][i]
+        frames[i][m] = rng.uniform(0.05, 99.99, m.sum()).astype(np.float32)
+    frames[2, :, 100:140] = 0  # empty column band
+    for blur in ("gaussian", "none"):
+        kw = {"blur_mode": blur, "fill_mode": "full"}
+        res = P.complete_batch(frames, _pcfg(P, kw))
+        got = res.dense.cpu().numpy()
+        for i in range(6):
+            ref, info = O.complete_with_stats(frames[i], _ocfg(kw))
+            _cmp(got[i], ref, blur)
+            assert int(res.iterations[i]) == info["large_fill_iterations"]

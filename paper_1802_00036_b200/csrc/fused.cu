@@ -19,8 +19,10 @@
 //   Producer (registers + shuffles): invert -> cross3 -> cross3 (= 5x5
 //   diamond) -> max5 -> min5 (close) -> masked max7 (small fill) -> extend.
 //   Stage-5 rows go to a 40-row shared-memory ring; the consumer runs 16 rows
-//   behind: 31x31 masked large fill (warp-cooperative, only for blocks that
-//   hold an empty pixel), 5x5 Gaussian (fp32), invert back, coalesced store.
+//   behind: 31x31 masked large fill (one warp-wide pass per empty pixel:
+//   lanes take the 31 window columns, redux.max combines them; typical
+//   frames hold ~50-200 such pixels), 5x5 Gaussian (fp32), invert back,
+//   coalesced store.
 //   Once the stage-5 rows are above every owned column's r0, stages 1-4 and
 //   the input reads stop: those rows are the captured top values.
 // Frames that still hold empties after one large-fill iteration are flagged
@@ -53,7 +55,6 @@ constexpr int kLag = 16;               // consumer lag behind the stage-5 produc
 constexpr int kPLag = 9;               // stage-5 lag behind the input: 1+1+2+2+3
 constexpr int kCLag = kPLag + kLag;    // consumer rows = t0 - 25 + j
 constexpr int kKFirst = (kCLag - 1 + kB - 1) / kB;  // first consumer block (needs rows <= +15 produced)
-constexpr int kVC = 160;               // large-fill scratch columns per warp (128 + 2*15, padded)
 constexpr int kLF = 15;                // large fill radius
 constexpr int kStripMax = 1248;        // widest strip handled by one CTA
 constexpr float kFMax = 3.402823466e38f;
@@ -379,57 +380,28 @@ __device__ __forceinline__ void phase1(const float* frame, const Params& p, int 
 }
 
 // ---------------------------------------------------------------------------
-// Large masked fill, step A (warp-cooperative): V[j][sc] = max over ring rows
-// [c_j - 15, c_j + 15] (clamped == clipped for max) at column L - 15 + sc.
-// Consecutive centres c_j = c0 + j share rows [c0-12, c0+15].
+// Large masked fill of one empty pixel (x, row), warp-cooperative: lane i
+// takes column x - 15 + i (i < 31) and the max over ring rows [row-15,
+// row+15] (clamped == clipped for max); columns outside [p0, p1) lie outside
+// the frame (the strip's ring covers every needed window) and count as 0.
+// Stage-5 values are >= 0, so their float bit patterns order like the values
+// and one redux.max combines the lanes.
 // ---------------------------------------------------------------------------
-__device__ __noinline__ void lf_vstep(const float* __restrict__ ring, int ringw, int p0, int p1, int H, int L,
-                                      int lane, int c0, bool consecutive, float* __restrict__ V) {
-#pragma unroll 1
-  for (int i = 0; i < kVC / 32; ++i) {
-    const int sc = lane + 32 * i;
-    const int col = L - kLF + sc;
-    float o[4] = {0.f, 0.f, 0.f, 0.f};
-    if (col >= p0 && col < p1) {
-      const float* rc = ring + (col - p0);
-      auto ld = [&](int r) {
-        const int rr = r < 0 ? 0 : (r >= H ? H - 1 : r);
-        return rc[((rr + kPLag) % kRing) * ringw];
-      };
-      if (consecutive) {
-        float core = ld(c0 - 12);
-#pragma unroll 9
-        for (int r = c0 - 11; r <= c0 + 15; ++r) core = fmx(core, ld(r));
-        const float u15 = ld(c0 - 15), u14 = ld(c0 - 14), u13 = ld(c0 - 13);
-        const float d16 = ld(c0 + 16), d17 = ld(c0 + 17), d18 = ld(c0 + 18);
-        o[0] = fmx(core, fmx3(u15, u14, u13));
-        o[1] = fmx3(core, fmx(u14, u13), d16);
-        o[2] = fmx3(core, u13, fmx(d16, d17));
-        o[3] = fmx(core, fmx3(d16, d17, d18));
-      } else {  // frame ends: each row centre clamped separately
-#pragma unroll
-        for (int j = 0; j < kB; ++j) {
-          const int cj = min(max(c0 + j, 0), H - 1);
-          float m = ld(cj - kLF);
-#pragma unroll 5
-          for (int r = cj - kLF + 1; r <= cj + kLF; ++r) m = fmx(m, ld(r));
-          o[j] = m;
-        }
-      }
+__device__ __forceinline__ float lf_one(const float* __restrict__ ring, int ringw, int p0, int p1, int H, int lane,
+                                        int x, int row) {
+  const int col = x - kLF + lane;
+  unsigned m = 0u;
+  if (lane < 2 * kLF + 1 && col >= p0 && col < p1) {
+    const float* rc = ring + (col - p0);
+    const int r0 = max(row - kLF, 0), r1 = min(row + kLF, H - 1);
+    int slot = (r0 + kPLag) % kRing;
+#pragma unroll 8
+    for (int r = r0; r <= r1; ++r) {
+      m = max(m, __float_as_uint(rc[slot * ringw]));
+      slot = slot + 1 == kRing ? 0 : slot + 1;
     }
-#pragma unroll
-    for (int j = 0; j < kB; ++j) V[j * kVC + sc] = o[j];
   }
-  __syncwarp();
-}
-
-// step B: max over scratch row j, columns [4*lane + c, 4*lane + c + 30]  (<-> x-15 .. x+15)
-__device__ __forceinline__ float lf_pixel(const float* __restrict__ V, int j, int lane, int c) {
-  const float* vr = V + j * kVC + 4 * lane + c;
-  float m = vr[0];
-#pragma unroll 10
-  for (int d = 1; d <= 2 * kLF; ++d) m = fmx(m, vr[d]);
-  return m;
+  return __uint_as_float(__reduce_max_sync(kFull, m));
 }
 
 // ---------------------------------------------------------------------------
@@ -441,7 +413,6 @@ struct State {
   const float* rring;  // consumer read base: ring + clamped lane column
   float* wring;        // producer write base: ring + lane column (owned lanes only)
   float* ring;
-  float* V;
   int ringw, x0, lane, L, p0, p1;
   unsigned own, outm, oob, oobL, oobR;
   bool woob;
@@ -619,24 +590,33 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
   }
   if (FULL) {
     // any needed empty pixel in this block? (max with nb masks unneeded columns)
-    float mn = kFMax;
+    unsigned em = 0;  // bit 4j+c: needed empty pixel
 #pragma unroll
     for (int j = 0; j < kB; ++j)
 #pragma unroll
-      for (int c = 0; c < 4; ++c) mn = fminf(mn, fmaxf(v6[j].v[c], S.nb[c]));
-    const bool e = !(mn > kValid);
-    if (__any_sync(kFull, e)) {
-      S.had_empty |= e;
-      lf_vstep(S.ring, S.ringw, S.p0, S.p1, H, S.L, S.lane, tc0, !EDGE || (tc0 >= 0 && tc0 + kB - 1 < H), S.V);
+      for (int c = 0; c < 4; ++c) em |= (unsigned)!(fmaxf(v6[j].v[c], S.nb[c]) > kValid) << (4 * j + c);
+    unsigned lanes = __ballot_sync(kFull, em != 0);
+    if (lanes) {
+      S.had_empty |= em != 0;
+      do {
+        const int src = __ffs(lanes) - 1;
+        lanes &= lanes - 1;
+        unsigned pe = __shfl_sync(kFull, em, src);
+        do {
+          const int b = __ffs(pe) - 1;
+          pe &= pe - 1;
+          const int row = EDGE ? min(max(tc0 + (b >> 2), 0), H - 1) : tc0 + (b >> 2);
+          const float r = lf_one(S.ring, S.ringw, S.p0, S.p1, H, S.lane, S.L + 4 * src + (b & 3), row);
+          if (S.lane == src) {
 #pragma unroll
-      for (int j = 0; j < kB; ++j)
+            for (int j = 0; j < kB; ++j)
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-          if (!(fmaxf(v6[j].v[c], S.nb[c]) > kValid)) {
-            v6[j].v[c] = lf_pixel(S.V, j, S.lane, c);
-            S.still_empty |= !(v6[j].v[c] > kValid);
+              for (int c = 0; c < 4; ++c)
+                if (b == 4 * j + c) v6[j].v[c] = r;
+            S.still_empty |= !(r > kValid);
           }
-      __syncwarp();
+        } while (pe);
+      } while (lanes);
     }
   }
   // out-of-frame columns replicate the edge column (the blur needs true replicate)
@@ -731,7 +711,6 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
     State S;
     S.ringw = ((g.p1 - g.p0) + 3) & ~3;
     S.ring = smem;
-    S.V = smem + kRing * S.ringw + warp * (kB * kVC);
     S.src = p.in + frame * HW;
     S.dst = p.out + frame * HW;
     S.x0 = g.L + 4 * lane;
@@ -859,7 +838,7 @@ __global__ void finalize_kernel(const float* __restrict__ in, int64_t HW, const 
 }
 
 struct Layout {
-  int strips, SW, nw;
+  int strips, SW, nw, per_sm;  // per_sm: resident CTAs per SM (1)
   size_t smem;
 };
 
@@ -876,16 +855,11 @@ int host_warps(int o0, int o1, int W) {
   return nw;
 }
 
-Layout layout(int W) {
+Layout layout_for(int W, int strips) {
   Layout L;
-  if (W <= kStripMax) {
-    L.strips = 1;
-    L.SW = W;
-  } else {
-    L.strips = (W + 1023) / 1024;
-    L.SW = (((W + L.strips - 1) / L.strips) + 3) & ~3;
-    L.strips = (W + L.SW - 1) / L.SW;
-  }
+  L.strips = strips;
+  L.SW = strips == 1 ? W : (((W + strips - 1) / strips) + 3) & ~3;
+  L.strips = (W + L.SW - 1) / L.SW;
   L.nw = 0;
   int pwmax = 0;
   for (int s = 0; s < L.strips; ++s) {
@@ -896,9 +870,15 @@ Layout layout(int W) {
     pwmax = std::max(pwmax, p1 - p0);
   }
   const int ringw = (pwmax + 3) & ~3;
-  L.smem = (size_t)kRing * ringw * 4 + (size_t)L.nw * kB * kVC * 4;
+  L.smem = (size_t)kRing * ringw * 4;
+  L.per_sm = 1;
   return L;
 }
+
+// One CTA per strip of <= 1248 columns (a whole 1216- or 1242-wide frame).
+// Splitting such frames into two 6-warp CTAs per SM measured slower (the
+// strip halos and phase 1 are paid twice).
+Layout layout(int W) { return layout_for(W, W <= kStripMax ? 1 : (W + 1023) / 1024); }
 
 template <int VEC, bool FULL, int BLUR>
 cudaError_t launch_t(const Params& p, size_t smem, int grid, cudaStream_t s) {
@@ -961,7 +941,8 @@ cudaError_t launch_fused(const float* in, float* out, int64_t B, int H, int W, c
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t items = B * L.strips;
-  const int grid = (int)(items < sms ? items : sms);
+  const int64_t slots = (int64_t)sms * L.per_sm;
+  const int grid = (int)(items < slots ? items : slots);
   const int vec = (W % 4 == 0) ? 4 : ((W % 2 == 0) ? 2 : 1);
   const bool full = c.fill_mode == DFC_FILL_FULL;
   const bool gauss = c.blur_mode == DFC_BLUR_GAUSSIAN;

@@ -224,6 +224,67 @@ __device__ __forceinline__ void store4(float* row, int x0, const F4& a, unsigned
     if (colmask & (1u << c)) __stcs(row + x0 + c, a.v[c]);
 }
 
+// q points at the lane's first column of a row
+template <int VEC>
+__device__ __forceinline__ void store_lane(float* q, const F4& a, unsigned colmask) {
+  if (colmask == 0xFu) {
+    if constexpr (VEC == 4) {
+      __stcs(reinterpret_cast<float4*>(q), make_float4(a.v[0], a.v[1], a.v[2], a.v[3]));
+      return;
+    } else if constexpr (VEC == 2) {
+      __stcs(reinterpret_cast<float2*>(q), make_float2(a.v[0], a.v[1]));
+      __stcs(reinterpret_cast<float2*>(q + 2), make_float2(a.v[2], a.v[3]));
+      return;
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    if (colmask & (1u << c)) __stcs(q + c, a.v[c]);
+}
+
+// Stage one lane's 4 columns of an input row into shared memory with cp.async
+// (zero-filled where the row or the columns lie outside the frame).
+template <int BYTES>
+__device__ __forceinline__ void cp_async_zfill(uint32_t sdst, const void* gsrc, bool ok) {
+  const int n = ok ? BYTES : 0;
+  if constexpr (BYTES == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sdst), "l"(gsrc), "r"(n) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(sdst), "l"(gsrc), "n"(BYTES), "r"(n)
+                 : "memory");
+}
+
+template <int VEC>
+__device__ __forceinline__ void stage_lane(uint32_t sdst, const float* q, const float* safe, bool rowok, bool full,
+                                           unsigned incol) {
+  if constexpr (VEC == 4) {
+    const bool ok = rowok && full;
+    cp_async_zfill<16>(sdst, ok ? q : safe, ok);
+  } else if constexpr (VEC == 2) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const bool ok = rowok && ((incol >> (2 * h)) & 3u) == 3u;
+      cp_async_zfill<8>(sdst + 8 * h, ok ? q + 2 * h : safe, ok);
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const bool ok = rowok && (incol >> c & 1);
+      cp_async_zfill<4>(sdst + 4 * c, ok ? q + c : safe, ok);
+    }
+  }
+}
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+__device__ __forceinline__ F4 lds4(uint32_t saddr) {
+  float4 q;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n" : "=f"(q.x), "=f"(q.y), "=f"(q.z), "=f"(q.w) : "r"(saddr)
+               : "memory");
+  return F4{{q.x, q.y, q.z, q.w}};
+}
+
 // ---------------------------------------------------------------------------
 // per-item warp geometry
 // ---------------------------------------------------------------------------
@@ -408,8 +469,6 @@ __device__ __forceinline__ float lf_one(const float* __restrict__ ring, int ring
 // per-item state and one 4-row iteration (EDGE: rows may leave the frame)
 // ---------------------------------------------------------------------------
 struct State {
-  const float* src;
-  float* dst;
   const float* rring;  // consumer read base: ring + clamped lane column
   float* wring;        // producer write base: ring + lane column (owned lanes only)
   float* ring;
@@ -420,8 +479,16 @@ struct State {
   int T0[4];
   float top[4];
   int tmin, tmax;
-  bool skip;
-  F4 c1[2], c2[2], c3[4], c4[4], c5[6], gc[4], mprev[2], nx[kB];
+  int tmaxN;           // max r0 row (processing order) over the columns the consumer needs
+  bool skip, fast;
+  F4 c1[2], c2[2], c3[4], c4[4], c5[6], gc[4], mprev[2];
+  F4 ofast;            // output row above every needed r0 (FULL): all such rows are equal
+  uint32_t stg;        // shared-memory staging slot of this lane (row j at +512 j)
+  const float* lrow;   // input row of processing row t0 + kB at column x0
+  float* orow;         // output row of processing row tc0 - 2 at column x0
+  bool full;           // all 4 columns inside the frame
+  unsigned incol;
+  float amin;          // FULL: min blurred value (<= 0.1 sends the frame to the staged path)
   unsigned umax;
   bool had_empty, still_empty;
   int srcL, srcR, compR;  // replicate sources for out-of-frame columns
@@ -437,9 +504,10 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
   F4 f[kB];
   if (!S.skip) {
     F4 a[kB];
+    cp_async_wait_all();  // this block's rows, staged one block ago
 #pragma unroll
     for (int j = 0; j < kB; ++j) {
-      a[j] = S.nx[j];
+      a[j] = lds4(S.stg + j * 512);
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const float v = a[j].v[c];
@@ -447,15 +515,16 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
         a[j].v[c] = v > kValid ? p.md - v : 0.0f;
       }
     }
-    // prefetch the next block; stops once its stage-5 rows lie above every r0
-    const bool next_needed = !FULL || (t0 + kB - kPLag <= S.tmax);
+    // stage the next block; stops once its stage-5 rows lie above every r0.
+    // umax depends on every staged value: the shared reads are complete
+    // before the slot is overwritten.
+    asm volatile("" ::"r"(S.umax));
+    if (!FULL || (t0 + kB - kPLag <= S.tmax)) {
+      const float* q = S.lrow;
 #pragma unroll
-    for (int j = 0; j < kB; ++j) {
-      const int t = t0 + kB + j;
-      if ((!EDGE || t < H) && next_needed)
-        S.nx[j] = load4<VEC, true>(S.src + (int64_t)(H - 1 - t) * W, S.x0, W);
-      else
-        set_row(S.nx[j], 0.f);
+      for (int j = 0; j < kB; ++j, q -= W)
+        stage_lane<VEC>(S.stg + j * 512, q, p.in, !EDGE || t0 + kB + j < H, S.full, S.incol);
+      cp_async_commit();
     }
     // --- cross3 #1 (rows t0-1+j) ---
     F4 d1[kB];
@@ -561,6 +630,7 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
 #pragma unroll
       for (int c = 0; c < 4; ++c) f[j].v[c] = S.top[c];
   }
+  S.lrow -= kB * W;
   // --- ring store: ring slot of row t is (t + 9) mod 40, so this block is slots 4*(k mod 10) + j ---
   if (S.own) {
     float* w = S.wring + (k % kRingBlocks) * kB * S.ringw;
@@ -573,6 +643,19 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
   // ======================= consumer =======================
   const int tc0 = t0 - kCLag;
   if (k < kKFirst) return;
+  float* orow = S.orow;  // output row of processing row tc0 - 2
+  S.orow -= kB * W;
+  if (FULL && S.fast) {
+    // every row of the blur windows lies above each needed column's r0: the
+    // stage-6 rows are the captured top values and every output row is equal
+#pragma unroll
+    for (int j = 0; j < kB; ++j, orow -= W) {
+      const int t = tc0 - 2 + j;
+      if (EDGE && (t < 0 || t >= H)) continue;
+      if (S.outm) store_lane<VEC>(orow, S.ofast, S.outm);
+    }
+    return;
+  }
   F4 v6[kB];
   {
     // rows tc0 + j live in slots 4*((k + 6) mod 10) + j when inside the frame
@@ -590,14 +673,19 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
   }
   if (FULL) {
     // any needed empty pixel in this block? (max with nb masks unneeded columns)
-    unsigned em = 0;  // bit 4j+c: needed empty pixel
+    float mn = kFMax;
 #pragma unroll
     for (int j = 0; j < kB; ++j)
 #pragma unroll
-      for (int c = 0; c < 4; ++c) em |= (unsigned)!(fmaxf(v6[j].v[c], S.nb[c]) > kValid) << (4 * j + c);
-    unsigned lanes = __ballot_sync(kFull, em != 0);
-    if (lanes) {
+      for (int c = 0; c < 4; ++c) mn = fminf(mn, fmaxf(v6[j].v[c], S.nb[c]));
+    if (__any_sync(kFull, !(mn > kValid))) {
+      unsigned em = 0;  // bit 4j+c: needed empty pixel
+#pragma unroll
+      for (int j = 0; j < kB; ++j)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) em |= (unsigned)!(fmaxf(v6[j].v[c], S.nb[c]) > kValid) << (4 * j + c);
       S.had_empty |= em != 0;
+      unsigned lanes = __ballot_sync(kFull, em != 0);
       do {
         const int src = __ffs(lanes) - 1;
         lanes &= lanes - 1;
@@ -656,11 +744,11 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
       mk[0] = S.mprev[0], mk[1] = S.mprev[1], mk[2] = v6[0], mk[3] = v6[1];
       S.mprev[0] = v6[2], S.mprev[1] = v6[3];
     }
+    F4 o;
 #pragma unroll
-    for (int j = 0; j < kB; ++j) {
+    for (int j = 0; j < kB; ++j, orow -= W) {
       const int t = tc0 + j - 2;  // output row (processing order)
       if (EDGE && (t < 0 || t >= H)) continue;
-      F4 o;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         float a = p.gw[0] * in[j].v[c];
@@ -671,17 +759,27 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
         o.v[c] = a > kValid ? p.md - a : 0.0f;
         if (!FULL && !(mk[j].v[c] > kValid)) o.v[c] = 0.0f;
       }
-      if (S.outm) store4<VEC>(S.dst + (int64_t)(H - 1 - t) * W, S.x0, o, S.outm);
+      if (S.outm) store_lane<VEC>(orow, o, S.outm);
+    }
+    // rows tc0-4 .. tc0+3 above every needed r0: output row tc0+1 repeats from here on
+    if (FULL && !EDGE && tc0 - 4 > S.tmaxN) {
+      S.fast = true;
+      S.ofast = o;
     }
   } else {
+    orow -= 2 * W;  // no blur: output rows are tc0 + j
+    F4 o;
 #pragma unroll
-    for (int j = 0; j < kB; ++j) {
+    for (int j = 0; j < kB; ++j, orow -= W) {
       const int t = tc0 + j;
       if (EDGE && (t < 0 || t >= H)) continue;
-      F4 o;
 #pragma unroll
       for (int c = 0; c < 4; ++c) o.v[c] = v6[j].v[c] > kValid ? p.md - v6[j].v[c] : 0.0f;
-      if (S.outm) store4<VEC>(S.dst + (int64_t)(H - 1 - t) * W, S.x0, o, S.outm);
+      if (S.outm) store_lane<VEC>(orow, o, S.outm);
+    }
+    if (FULL && !EDGE && tc0 > S.tmaxN) {
+      S.fast = true;
+      S.ofast = o;
     }
   }
 }
@@ -711,8 +809,8 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
     State S;
     S.ringw = ((g.p1 - g.p0) + 3) & ~3;
     S.ring = smem;
-    S.src = p.in + frame * HW;
-    S.dst = p.out + frame * HW;
+    const float* src = p.in + frame * HW;
+    float* dst = p.out + frame * HW;
     S.x0 = g.L + 4 * lane;
     S.lane = lane;
     S.L = g.L;
@@ -720,7 +818,7 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
     S.p1 = g.p1;
     S.wring = S.ring + (S.x0 - g.p0);
     S.rring = S.ring + (min(max(S.x0, g.p0), g.p0 + S.ringw - 4) - g.p0);
-    unsigned incol = 0;
+    unsigned incol = 0, needm = 0;
     S.own = S.outm = S.oob = S.oobL = S.oobR = 0;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
@@ -732,7 +830,10 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
       S.outm |= (unsigned)(x >= max(g.q0, g.o0) && x < min(g.q1, g.o1)) << c;
       const bool need = x >= max(max(g.q0 - 2, g.o0 - 2), max(g.p0, 0)) && x < min(min(g.q1 + 2, g.o1 + 2), g.p1);
       S.nb[c] = need ? -kFMax : kFMax;
+      needm |= (unsigned)need << c;
     }
+    S.incol = incol;
+    S.full = incol == 0xFu;
     S.oob = S.oobL | S.oobR;
     S.woob = __any_sync(kFull, S.oob != 0);
     S.srcL = (0 - g.L) >> 2;  // lane holding column 0 (component 0)
@@ -742,23 +843,28 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
     S.srcR = min(max(S.srcR, 0), 31);
     S.umax = 0;
     S.had_empty = S.still_empty = false;
-    S.skip = false;
+    S.skip = S.fast = false;
+    S.tmaxN = INT_MAX;
+    set_row(S.ofast, 0.f);
 
     // ---------------- phase 1 ----------------
 #pragma unroll
     for (int c = 0; c < 4; ++c) S.T0[c] = INT_MAX, S.top[c] = 0.f;
     S.tmax = S.tmin = INT_MAX;
     if (FULL) {
-      phase1<VEC>(S.src, p, S.x0, S.own != 0, incol, S.T0, S.umax);
-      int mx = INT_MIN, mn = INT_MAX;
+      phase1<VEC>(src, p, S.x0, (S.own | needm) != 0, incol, S.T0, S.umax);
+      int mx = INT_MIN, mn = INT_MAX, mxn = INT_MIN;
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
+      for (int c = 0; c < 4; ++c) {
         if (S.own >> c & 1) {
           mx = max(mx, S.T0[c]);
           mn = min(mn, S.T0[c]);
         }
+        if (needm >> c & 1) mxn = max(mxn, S.T0[c]);
+      }
       S.tmax = __reduce_max_sync(kFull, mx);
       S.tmin = __reduce_min_sync(kFull, mn);
+      S.tmaxN = __reduce_max_sync(kFull, mxn);
     }
 
     // ---------------- phase 2 ----------------
@@ -768,9 +874,14 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
     for (int i = 0; i < 4; ++i) set_row(S.c3[i], 0.f), set_row(S.c4[i], kFMax), set_row(S.gc[i], 0.f);
 #pragma unroll
     for (int i = 0; i < 6; ++i) set_row(S.c5[i], 0.f);
+    S.stg = (uint32_t)__cvta_generic_to_shared(smem + kRing * S.ringw) + warp * (kB * 512) + lane * 16;
+    cp_async_wait_all();  // no copy of the previous item may still land in the slot
 #pragma unroll
     for (int j = 0; j < kB; ++j)
-      S.nx[j] = j < H ? load4<VEC, true>(S.src + (int64_t)(H - 1 - j) * W, S.x0, W) : F4{{0.f, 0.f, 0.f, 0.f}};
+      stage_lane<VEC>(S.stg + j * 512, src + (int64_t)(H - 1 - j) * W + S.x0, p.in, j < H, S.full, incol);
+    cp_async_commit();
+    S.lrow = src + (int64_t)(H - 1 - kB) * W + S.x0;
+    S.orow = dst + (int64_t)(H - 1 - (kB * kKFirst - kCLag - 2)) * W + S.x0;
 
     // iterations with every row inside the frame run the lean body
     const int K = (H + kCLag + 2) / kB + 1;
@@ -870,7 +981,7 @@ Layout layout_for(int W, int strips) {
     pwmax = std::max(pwmax, p1 - p0);
   }
   const int ringw = (pwmax + 3) & ~3;
-  L.smem = (size_t)kRing * ringw * 4;
+  L.smem = (size_t)kRing * ringw * 4 + (size_t)L.nw * kB * 512;
   L.per_sm = 1;
   return L;
 }

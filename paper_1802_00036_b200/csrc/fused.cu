@@ -73,6 +73,7 @@ struct Params {
   int H, W, strips, SW, nw;
   float md;
   float gw[5];
+  float2 gh[6];  // horizontal pass on column pairs: coefficients of e[i] for outputs (c, c+1)
   uint32_t* status;
   int32_t* iters;
   unsigned long long* nfallback;
@@ -724,12 +725,13 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
     for (int j = 0; j < kB; ++j) {
       const Ext<2> e = ext_row<2>(v6[j]);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        float a = p.gw[0] * e.e[c];
-        a = fmaf(p.gw[1], e.e[c + 1], a);
-        a = fmaf(p.gw[2], e.e[c + 2], a);
-        a = fmaf(p.gw[3], e.e[c + 3], a);
-        h[j].v[c] = fmaf(p.gw[4], e.e[c + 4], a);
+      for (int hp = 0; hp < 2; ++hp) {  // packed fp32x2: outputs (2hp, 2hp+1), inputs broadcast
+        const float* x = e.e + 2 * hp;
+        float2 a = __fmul2_rn(make_float2(x[0], x[0]), p.gh[0]);
+#pragma unroll
+        for (int i = 1; i < 6; ++i) a = __ffma2_rn(make_float2(x[i], x[i]), p.gh[i], a);
+        h[j].v[2 * hp] = a.x;
+        h[j].v[2 * hp + 1] = a.y;
       }
     }
     if (EDGE && k == kKFirst) {  // rows above row 0 replicate it (tc0 = -1: h[0] is row 0)
@@ -750,14 +752,17 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
       const int t = tc0 + j - 2;  // output row (processing order)
       if (EDGE && (t < 0 || t >= H)) continue;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        float a = p.gw[0] * in[j].v[c];
-        a = fmaf(p.gw[1], in[j + 1].v[c], a);
-        a = fmaf(p.gw[2], in[j + 2].v[c], a);
-        a = fmaf(p.gw[3], in[j + 3].v[c], a);
-        a = fmaf(p.gw[4], in[j + 4].v[c], a);
-        o.v[c] = a > kValid ? p.md - a : 0.0f;
+      for (int hp = 0; hp < 2; ++hp) {  // packed fp32x2 over the column pair (2hp, 2hp+1)
+        const int c = 2 * hp;
+        float2 a = __fmul2_rn(make_float2(in[j].v[c], in[j].v[c + 1]), make_float2(p.gw[0], p.gw[0]));
+#pragma unroll
+        for (int i = 1; i < 5; ++i)
+          a = __ffma2_rn(make_float2(in[j + i].v[c], in[j + i].v[c + 1]), make_float2(p.gw[i], p.gw[i]), a);
+        const float2 r = __ffma2_rn(a, make_float2(-1.f, -1.f), make_float2(p.md, p.md));  // md - a, exact negation
+        o.v[c] = a.x > kValid ? r.x : 0.0f;
+        o.v[c + 1] = a.y > kValid ? r.y : 0.0f;
         if (!FULL && !(mk[j].v[c] > kValid)) o.v[c] = 0.0f;
+        if (!FULL && !(mk[j].v[c + 1] > kValid)) o.v[c + 1] = 0.0f;
       }
       if (S.outm) store_lane<VEC>(orow, o, S.outm);
     }
@@ -1039,6 +1044,8 @@ cudaError_t launch_fused(const float* in, float* out, int64_t B, int H, int W, c
     for (int i = -r; i <= r; ++i) w[i + r] = std::exp(-(double)(i * i) / (2.0 * c.gaussian_sigma * c.gaussian_sigma));
     for (int i = 0; i < 5; ++i) sum += w[i];
     for (int i = 0; i < 5; ++i) p.gw[i] = (float)(w[i] / sum);
+    for (int i = 0; i < 6; ++i)
+      p.gh[i] = make_float2(i < 5 ? p.gw[i] : 0.f, i > 0 ? p.gw[i - 1] : 0.f);
   }
   p.status = status;
   p.iters = iters;

@@ -14,6 +14,10 @@ through the host-buffer API (pinned host in -> GPU -> pinned host out, copies
 inside the timed region).  ``--impl reference`` times the reference CPU path
 (oracle/_ref compiled reference kernels under the oracle orchestration, all
 host cores) on the same config.
+
+``--config N`` measures another BASELINE.json config the same way (0: partial
+fill + bilateral; 2/4: fill_in_multiscale with median + bilateral; 3: 1242x375);
+the driver's default run is config 1, the headline metric.
 """
 
 from __future__ import annotations
@@ -38,13 +42,30 @@ UNIT = "frames/s"
 CONFIG_ID = 1
 
 
+# BASELINE.json configs: (blur, fill, multiscale, default frames per GPU, call)
+CONFIGS = {
+    0: ("bilateral", "partial", False, 1024,
+        "fill_in_fast(max_depth=100, 5x5 diamond, extrapolate=False, blur_type='bilateral')"),
+    1: ("gaussian", "full", False, 1024,
+        "fill_in_fast(max_depth=100, 5x5 diamond, extrapolate=True, blur_type='gaussian')"),
+    2: ("median_bilateral", "full", True, 1024,
+        "fill_in_multiscale(max_depth=100, extrapolate=True, blur_type='bilateral', median_blur=True)"),
+    3: ("gaussian", "full", False, 1024,
+        "fill_in_fast(max_depth=100, 5x5 diamond, extrapolate=True, blur_type='gaussian')"),
+    4: ("median_bilateral", "full", True, 64,
+        "fill_in_multiscale(max_depth=120, extrapolate=True, blur_type='bilateral', median_blur=True)"),
+}
+
+
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--frames", type=int, default=1024, help="frames per rank per step")
+    p.add_argument("--config", type=int, default=1, choices=sorted(CONFIGS),
+                   help="BASELINE.json config (1 = the headline metric; the others are extra measurements)")
+    p.add_argument("--frames", type=int, default=None, help="frames per rank per step (default: per config)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU-baseline sample length")
@@ -73,7 +94,7 @@ def gen_frames(start, count, procs=None):
     from paper_1802_00036_b200 import synth
 
     procs = procs or max(1, min(16, (os.cpu_count() or 1)))
-    spec = synth.CONFIG_SPECS[CONFIG_ID]
+    spec = synth.CONFIG_SPECS[CONFIG_ID]  # set by main() from --config
     out = np.empty((count, spec.height, spec.width), dtype=np.float32)
     step = max(1, (count + procs - 1) // procs)
     parts = [(start + a, min(count - a, step)) for a in range(0, count, step)]
@@ -140,12 +161,24 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def oracle_config():
+    """The CPU restatement's config for the selected BASELINE config (same fields as the GPU arm)."""
+    from oracle import depthfill_oracle as O
+    from paper_1802_00036_b200 import synth
+
+    blur, fill, multi = CONFIGS[CONFIG_ID][:3]
+    ms = None
+    if multi:
+        ms = ((15.0, 30.0), (O.KernelShape.FULL, 7), (O.KernelShape.DIAMOND, 7), (O.KernelShape.DIAMOND, 5))
+    return O.OracleConfig(blur_mode=O.BlurMode(blur), fill_mode=O.FillMode(fill),
+                          max_depth=float(synth.CONFIG_SPECS[CONFIG_ID].max_depth), multiscale=ms)
+
+
 def cpu_baseline_leg(frames, seconds):
     """Reference CPU path on a bounded sample of the same workload, all host cores."""
     from oracle import cpu_baseline as C
-    from oracle import depthfill_oracle as O
 
-    cfg = O.OracleConfig(blur_mode=O.BlurMode.GAUSSIAN, fill_mode=O.FillMode.FULL)
+    cfg = oracle_config()
     kind = C.available_kind()
     one = C.single_frame_seconds(frames[0], cfg, kind)
     procs = os.cpu_count() or 1
@@ -153,7 +186,7 @@ def cpu_baseline_leg(frames, seconds):
     sample = frames[: min(len(frames), 256)]
     r = C.time_cpu(sample, cfg, n, procs, kind)
     return {"value": round(r["value"], 3), "unit": UNIT, "cores": r["cores"], "kind": kind,
-            "sample": f"{n} config-1 frames (cycling over {len(sample)} distinct) on {procs} worker processes, "
+            "sample": f"{n} config-{CONFIG_ID} frames (cycling over {len(sample)} distinct) on {procs} worker processes, "
                       f"1 thread each; {r['seconds']:.1f} s; single-thread {one * 1e3:.1f} ms/frame",
             "cpu_model": _cpu_model()}
 
@@ -169,10 +202,15 @@ def _cpu_model():
 
 
 def config_block(B, args):
-    return {"workload": f"BASELINE config 1: fill_in_fast(max_depth=100, 5x5 diamond, extrapolate=True, "
-                        f"blur_type='gaussian') on {B} synthetic 1216x352 frames per GPU",
-            "frames_per_gpu": B, "width": 1216, "height": 352, "density": "U(4%,6%)",
-            "l2": "no flush needed: each step streams 2 x %.2f GB (> 126 MB L2)" % (B * 1216 * 352 * 4 / 1e9),
+    from paper_1802_00036_b200 import synth
+
+    sp = synth.CONFIG_SPECS[CONFIG_ID]
+    dens = (f"{sp.density[0]:.0%}" if sp.density[0] == sp.density[1]
+            else f"U({sp.density[0]:.0%},{sp.density[1]:.0%})")
+    return {"workload": f"BASELINE config {CONFIG_ID}: {CONFIGS[CONFIG_ID][4]} on {B} synthetic "
+                        f"{sp.width}x{sp.height} frames per GPU",
+            "config_id": CONFIG_ID, "frames_per_gpu": B, "width": sp.width, "height": sp.height, "density": dens,
+            "l2": "no flush needed: each step streams 2 x %.2f GB (> 126 MB L2)" % (B * sp.width * sp.height * 4 / 1e9),
             "parallelism": f"frame-sharded dp{args.gpus}, no collective",
             "path": ("reference CPU (oracle/_ref compiled reference kernels)" if args.impl == "reference"
                      else ("staged" if args.force_staged else "fused"))}
@@ -183,10 +221,9 @@ def run_reference(args):
     if rank != 0:
         return
     from oracle import cpu_baseline as C
-    from oracle import depthfill_oracle as O
 
-    frames = gen_frames(0, 64)
-    cfg = O.OracleConfig(blur_mode=O.BlurMode.GAUSSIAN, fill_mode=O.FillMode.FULL)
+    frames = gen_frames(0, 64 if CONFIG_ID != 4 else 8)
+    cfg = oracle_config()
     procs = os.cpu_count() or 1
     pool, procs, kind = C.make_pool(frames, cfg, procs)
     per_step = 2 * procs
@@ -207,7 +244,7 @@ def run_reference(args):
             "impl": "reference",
             "config": {**config_block(args.frames, args), "reference_step": f"{per_step} frames per step"},
             "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": procs, "kind": kind,
-                             "sample": f"{per_step} frames/step x {args.steps} steps over 64 distinct frames",
+                             "sample": f"{per_step} frames/step x {args.steps} steps over {len(frames)} distinct frames",
                              "cpu_model": _cpu_model()},
             "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -225,6 +262,12 @@ def run_ours(args):
 
     from paper_1802_00036_b200.sharding import env_rank_world, frame_range, max_over_ranks
 
+    from paper_1802_00036_b200 import synth
+    from paper_1802_00036_b200.completion import MultiscaleConfig
+
+    spec = synth.CONFIG_SPECS[CONFIG_ID]
+    H, W = spec.height, spec.width
+    blur, fill, multi = CONFIGS[CONFIG_ID][:3]
     rank, local, world = env_rank_world()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -237,11 +280,12 @@ def run_ours(args):
     out = torch.empty_like(x)
     status = torch.empty(B, dtype=torch.int32, device=dev)
     iters = torch.empty(B, dtype=torch.int32, device=dev)
-    config = PipelineConfig(blur_mode=BlurMode.GAUSSIAN, fill_mode=FillMode.FULL, max_depth=100.0)
-    cfg = to_dfc_config(config, force_staged=args.force_staged)
+    config = PipelineConfig(blur_mode=BlurMode(blur), fill_mode=FillMode(fill), max_depth=float(spec.max_depth))
+    ms = MultiscaleConfig() if multi else None
+    cfg = to_dfc_config(config, multiscale=ms, force_staged=args.force_staged)
     cfg.flags |= _lib.F_NO_FINISH
     L = _lib.load()
-    need = int(L.dfc_workspace_bytes(ctypes.byref(cfg), B, 352, 1216))
+    need = int(L.dfc_workspace_bytes(ctypes.byref(cfg), B, H, W))
     ws = torch.empty(need, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
     sp = ctypes.c_void_p(stream.cuda_stream)
@@ -250,18 +294,18 @@ def run_ours(args):
     def step(ev0=None, ev1=None):
         if ev0 is not None:
             ev0.record(stream)
-        _lib.check(L.dfc_fill_batch(P(x), P(out), B, 352, 1216, ctypes.byref(cfg), P(status), P(iters), P(ws),
+        _lib.check(L.dfc_fill_batch(P(x), P(out), B, H, W, ctypes.byref(cfg), P(status), P(iters), P(ws),
                                     ws.numel(), sp))
         if ev1 is not None:
             ev1.record(stream)
-        _lib.check(L.dfc_fill_finish(P(x), P(out), B, 352, 1216, ctypes.byref(cfg), P(status), P(iters), P(ws),
+        _lib.check(L.dfc_fill_finish(P(x), P(out), B, H, W, ctypes.byref(cfg), P(status), P(iters), P(ws),
                                      ws.numel(), sp))
 
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
     st = status.cpu().numpy()
-    raise_for_status(st, 100.0)
+    raise_for_status(st, float(spec.max_depth))
     n_fallback = int(np.count_nonzero(st & _lib.ST_FALLBACK))
 
     clocks = ClockSampler(local)
@@ -291,7 +335,7 @@ def run_ours(args):
     # ---- e2e: host buffers through the public API -------------------------
     e2e = None
     if not args.no_e2e:
-        pipe = HostPipeline(config, chunk=64)
+        pipe = HostPipeline(config, multiscale=ms, chunk=64 if W * H < 1 << 20 else 8)
         h_in = torch.from_numpy(host).pin_memory()
         h_out = torch.empty_like(h_in).pin_memory()
         for _ in range(2):
@@ -308,13 +352,14 @@ def run_ours(args):
         (dt,) = max_over_ranks([dt], device=dev)
         e2e = {"value": round(world * B * e_steps / dt, 3), "unit": UNIT,
                "h2d_bytes_per_step": int(h_in.numel() * 4) * world, "d2h_bytes_per_step": int(h_out.numel() * 4) * world,
-               "path": "pinned host -> H2D -> dfc_fill_batch -> D2H, 64-frame chunks on 3 streams, wall clock"}
+               "path": f"pinned host -> H2D -> dfc_fill_batch -> D2H, {pipe.chunk}-frame chunks on 3 streams, "
+                       "wall clock"}
         ok = bool(torch.equal(h_out, out.cpu()))
         e2e["matches_device_path"] = ok
 
     # ---- roofline of the dominant kernel ---------------------------------
     pk, pk_src = hbm_peak()
-    alg_bytes = 8 * 1216 * 352 * B  # one f32 read + one f32 write per pixel
+    alg_bytes = 8 * W * H * B  # one f32 read + one f32 write per pixel
     achieved = alg_bytes / (kern_ms / 1e3) / 1e9
     traffic = None
     tf = ROOT / "profiles" / "traffic.json"
@@ -351,7 +396,11 @@ def run_ours(args):
 
 
 def main():
+    global CONFIG_ID
     args = parse()
+    CONFIG_ID = args.config
+    if args.frames is None:
+        args.frames = CONFIGS[CONFIG_ID][3]
     if args.impl == "reference":
         run_reference(args)
     else:

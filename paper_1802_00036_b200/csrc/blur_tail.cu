@@ -1,0 +1,212 @@
+// Blur tail: stage 7 + stage 8 of the pipeline in one tiled kernel.
+//
+//   [median KxK] -> [Gaussian | bilateral KxK] -> [partial re-impose] -> invert back
+//
+// (pipeline._blur_stage, pipeline.py:206-238; morphology.py:99-125;
+// depth_core.invert_back :150-156.)  Input: the stage-6 (FULL) or stage-4
+// (PARTIAL) map in the inverted encoding; output: the final direct-depth map.
+// One CTA per 64x32 output tile: the input tile (+ median and blur halos,
+// replicate-clamped) is staged in shared memory, the median is computed on
+// the tile plus the blur halo -- each halo position at its frame-clamped
+// centre, which is exactly the replicate border the reference's blur sees --
+// then the blur, re-impose and re-inversion run per output pixel.
+//
+// The median is exact (selection network, bit-identical to the reference's
+// median_network).  The Gaussian is fp32 centre-relative c + sum w_i w_j (q - c) and the
+// bilateral fp32 centre-relative c + sum w (q - c) / sum w with exp2; both are
+// within the 1e-4 m bar of the float64 reference (tests/test_gpu_pipeline.py).
+// The exact float64 blurs (DFC_F_EXACT_BLUR) stay on the staged op kernels.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+
+#include "dfc_common.cuh"
+#include "median_networks.cuh"
+
+namespace dfc {
+namespace {
+
+constexpr int kTX = 64, kTY = 32, kThreads = 256;
+constexpr int kPostNone = 0, kPostGauss = 1, kPostBilateral = 2;
+
+struct TailParams {
+  float md;
+  float w2[25];  // Gaussian 2-D taps w_i * w_j (row-major, radius PR)
+  float ks[25];  // bilateral: log2(e) * spatial exponent per tap (dy^2 + dx^2) / (-2 sigma_s^2)
+  float kv;      // bilateral: log2(e) / (-2 sigma_v^2)
+};
+
+#define DFC_CSWAP(a, b)            \
+  do {                             \
+    const float lo_ = fminf(a, b); \
+    const float hi_ = fmaxf(a, b); \
+    a = lo_;                       \
+    b = hi_;                       \
+  } while (0)
+
+template <int MR>
+__device__ __forceinline__ float median_at(const float* __restrict__ t, int stride) {
+  // t points at the window's top-left element
+  constexpr int S = 2 * MR + 1;
+  float v[S * S];
+#pragma unroll
+  for (int dy = 0; dy < S; ++dy)
+#pragma unroll
+    for (int dx = 0; dx < S; ++dx) v[dy * S + dx] = t[dy * stride + dx];
+  if constexpr (S == 3) {
+    DFC_MEDNET9_APPLY(v);
+  } else {
+    DFC_MEDNET25_APPLY(v);
+  }
+  return v[(S * S) / 2];
+}
+
+template <int MR, int POST, int PR, bool PARTIAL>
+__global__ void __launch_bounds__(kThreads) blur_tail_kernel(const float* __restrict__ in, float* __restrict__ out,
+                                                             int H, int W, const __grid_constant__ TailParams p) {
+  constexpr int HI = MR + PR;                      // input halo
+  constexpr int IW = kTX + 2 * HI, IH = kTY + 2 * HI;
+  constexpr int MW = kTX + 2 * PR, MH = kTY + 2 * PR;
+  __shared__ float sIn[IH * IW];
+  __shared__ float sM[MH * MW];
+  const int64_t b = blockIdx.z;
+  const int x0 = blockIdx.x * kTX, y0 = blockIdx.y * kTY;
+  const float* src = in + b * (int64_t)H * W;
+  float* dst = out + b * (int64_t)H * W;
+
+  for (int i = threadIdx.x; i < IH * IW; i += kThreads) {
+    const int iy = i / IW, ix = i - iy * IW;
+    sIn[i] = __ldg(src + (int64_t)clampi(y0 - HI + iy, H) * W + clampi(x0 - HI + ix, W));
+  }
+  __syncthreads();
+
+  // stage-7a: median (or copy) on the tile + blur halo, at frame-clamped centres
+  for (int i = threadIdx.x; i < MH * MW; i += kThreads) {
+    const int my = i / MW, mx = i - my * MW;
+    const int cy = clampi(y0 - PR + my, H) - y0 + HI;  // centre in sIn coordinates
+    const int cx = clampi(x0 - PR + mx, W) - x0 + HI;
+    const float c = sIn[cy * IW + cx];
+    float v = c;
+    if constexpr (MR > 0) {
+      v = median_at<MR>(sIn + (cy - MR) * IW + (cx - MR), IW);
+      if (PARTIAL && !(c > kValid)) v = 0.0f;
+    }
+    sM[i] = v;
+  }
+  __syncthreads();
+
+  // stage-7b: Gaussian / bilateral, re-impose, invert back
+  for (int i = threadIdx.x; i < kTX * kTY; i += kThreads) {
+    const int oy = i / kTX, ox = i - oy * kTX;
+    const int gy = y0 + oy, gx = x0 + ox;
+    if (gy >= H || gx >= W) continue;
+    const float* m = sM + oy * MW + ox;  // window top-left (radius PR)
+    const float c = m[PR * MW + PR];
+    float r = c;
+    if constexpr (POST == kPostGauss) {
+      // centre-relative: constant neighbourhoods come out exactly constant
+      float a = 0.0f;
+#pragma unroll
+      for (int dy = 0; dy <= 2 * PR; ++dy)
+#pragma unroll
+        for (int dx = 0; dx <= 2 * PR; ++dx) a = fmaf(p.w2[dy * (2 * PR + 1) + dx], m[dy * MW + dx] - c, a);
+      r = c + a;
+    } else if constexpr (POST == kPostBilateral) {
+      float acc = 0.0f, den = 0.0f;
+#pragma unroll
+      for (int dy = 0; dy <= 2 * PR; ++dy)
+#pragma unroll
+        for (int dx = 0; dx <= 2 * PR; ++dx) {
+          const float d = m[dy * MW + dx] - c;
+          const float w = exp2f(fmaf(p.kv * d, d, p.ks[dy * (2 * PR + 1) + dx]));
+          acc = fmaf(w, d, acc);
+          den += w;
+        }
+      r = c + acc / den;
+    }
+    if (PARTIAL && POST != kPostNone && !(c > kValid)) r = 0.0f;
+    __stcs(dst + (int64_t)gy * W + gx, r > kValid ? p.md - r : 0.0f);
+  }
+}
+
+template <int MR, int POST, int PR>
+cudaError_t launch_t(const float* in, float* out, int64_t B, int H, int W, bool partial, const TailParams& p,
+                     cudaStream_t s) {
+  const dim3 grid((W + kTX - 1) / kTX, (H + kTY - 1) / kTY, (unsigned)B);
+  note_launch();
+  if (partial)
+    blur_tail_kernel<MR, POST, PR, true><<<grid, kThreads, 0, s>>>(in, out, H, W, p);
+  else
+    blur_tail_kernel<MR, POST, PR, false><<<grid, kThreads, 0, s>>>(in, out, H, W, p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool blur_tail_supported(const dfc_config& c) {
+  if (c.flags & DFC_F_EXACT_BLUR) return false;
+  const int bm = c.blur_mode;
+  const bool med = bm == DFC_BLUR_MEDIAN || bm == DFC_BLUR_MEDIAN_BILATERAL || bm == DFC_BLUR_MEDIAN_GAUSSIAN;
+  const bool gauss = bm == DFC_BLUR_GAUSSIAN || bm == DFC_BLUR_MEDIAN_GAUSSIAN;
+  const bool bil = bm == DFC_BLUR_BILATERAL || bm == DFC_BLUR_MEDIAN_BILATERAL;
+  if (med && c.median_size != 3 && c.median_size != 5) return false;
+  if (gauss && c.gaussian_size != 3 && c.gaussian_size != 5) return false;
+  if (bil && c.bilateral_size != 3 && c.bilateral_size != 5) return false;
+  return true;
+}
+
+// Blur stage + invert back for B frames (in: inverted map; out: direct depth).
+cudaError_t launch_blur_tail(const float* in, float* out, int64_t B, int H, int W, const dfc_config& c,
+                             cudaStream_t s) {
+  const int bm = c.blur_mode;
+  const bool med = bm == DFC_BLUR_MEDIAN || bm == DFC_BLUR_MEDIAN_BILATERAL || bm == DFC_BLUR_MEDIAN_GAUSSIAN;
+  const bool gauss = bm == DFC_BLUR_GAUSSIAN || bm == DFC_BLUR_MEDIAN_GAUSSIAN;
+  const bool bil = bm == DFC_BLUR_BILATERAL || bm == DFC_BLUR_MEDIAN_BILATERAL;
+  const bool partial = c.fill_mode == DFC_FILL_PARTIAL;
+  TailParams p{};
+  p.md = c.max_depth;
+  int pr = 0;
+  if (gauss) {
+    pr = c.gaussian_size / 2;
+    const int k = c.gaussian_size;
+    double w[5], sum = 0;
+    for (int i = -pr; i <= pr; ++i) w[i + pr] = std::exp(-(double)(i * i) / (2.0 * c.gaussian_sigma * c.gaussian_sigma));
+    for (int i = 0; i < k; ++i) sum += w[i];
+    for (int i = 0; i < k; ++i) w[i] /= sum;
+    for (int i = 0; i < k; ++i)
+      for (int j = 0; j < k; ++j) p.w2[i * k + j] = (float)(w[i] * w[j]);
+  } else if (bil) {
+    pr = c.bilateral_size / 2;
+    const int k = c.bilateral_size;
+    const double l2e = 1.4426950408889634;
+    for (int dy = -pr; dy <= pr; ++dy)
+      for (int dx = -pr; dx <= pr; ++dx)
+        p.ks[(dy + pr) * k + dx + pr] =
+            (float)(l2e * -(double)(dy * dy + dx * dx) / (2.0 * c.bilateral_sigma_space * c.bilateral_sigma_space));
+    p.kv = (float)(l2e * -1.0 / (2.0 * c.bilateral_sigma_value * c.bilateral_sigma_value));
+  }
+  const int mr = med ? c.median_size / 2 : 0;
+  const int post = gauss ? kPostGauss : (bil ? kPostBilateral : kPostNone);
+#define DFC_TAIL(MR, POST, PR) \
+  if (mr == MR && post == POST && pr == PR) return launch_t<MR, POST, PR>(in, out, B, H, W, partial, p, s);
+  DFC_TAIL(0, kPostNone, 0)
+  DFC_TAIL(1, kPostNone, 0)
+  DFC_TAIL(2, kPostNone, 0)
+  DFC_TAIL(0, kPostGauss, 1)
+  DFC_TAIL(0, kPostGauss, 2)
+  DFC_TAIL(1, kPostGauss, 1)
+  DFC_TAIL(1, kPostGauss, 2)
+  DFC_TAIL(2, kPostGauss, 1)
+  DFC_TAIL(2, kPostGauss, 2)
+  DFC_TAIL(0, kPostBilateral, 1)
+  DFC_TAIL(0, kPostBilateral, 2)
+  DFC_TAIL(1, kPostBilateral, 1)
+  DFC_TAIL(1, kPostBilateral, 2)
+  DFC_TAIL(2, kPostBilateral, 1)
+  DFC_TAIL(2, kPostBilateral, 2)
+#undef DFC_TAIL
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace dfc

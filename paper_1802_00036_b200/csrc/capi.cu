@@ -244,7 +244,12 @@ int run_staged(const float* in, float* out, int64_t B, int H, int W, const dfc_c
         DFC_CK(dfc::launch_masked_fill(cur, q.c, cur, n, s));
       }
     }
-    // 7. blur stage (pipeline._blur_stage :206-238)
+    // 7 + 8. blur stage (pipeline._blur_stage :206-238) and invert back, one tiled kernel
+    if (dfc::blur_tail_supported(c)) {
+      DFC_CK(dfc::launch_blur_tail(cur, y, C, H, W, c, s));
+      continue;
+    }
+    // exact float64 blurs: one op per launch
     const int bm = c.blur_mode;
     const bool partial = !full;
     if (bm == DFC_BLUR_MEDIAN || bm == DFC_BLUR_MEDIAN_BILATERAL || bm == DFC_BLUR_MEDIAN_GAUSSIAN) {

@@ -58,6 +58,11 @@ cudaError_t launch_iter_update(const int64_t* counts, int32_t* iters, int64_t B,
 cudaError_t launch_or_status(uint32_t* status, uint32_t bits, cudaStream_t s);
 cudaError_t launch_finalize_status(const int64_t* n_valid, uint32_t* status, int64_t B, cudaStream_t s);
 
+// ---- blur stage + invert back in one tiled kernel (blur_tail.cu) ---------
+bool blur_tail_supported(const dfc_config& c);
+cudaError_t launch_blur_tail(const float* in, float* out, int64_t B, int H, int W, const dfc_config& c,
+                             cudaStream_t s);
+
 // ---- fused pipeline (fused.cu) -------------------------------------------
 struct FusedPlan;
 bool fused_supported(const dfc_config& c, int H, int W);

@@ -59,6 +59,8 @@ constexpr int kLF = 15;                // large fill radius
 constexpr int kStripMax = 1248;        // widest strip handled by one CTA
 constexpr float kFMax = 3.402823466e38f;
 constexpr uint32_t kNeedsStaged = 0x200u;  // internal status bit (capi.cu)
+constexpr int kBlurRaw = -1;           // emit the stage-6 (FULL) / stage-4 (PARTIAL) inverted map for blur_tail.cu
+constexpr int64_t kRawChunk = 296;     // frames per fused -> blur-tail round (2 per SM) in the raw mode
 
 static_assert(kRing % kB == 0 && kLag % kB == 0, "ring blocks must not wrap inside a block");
 
@@ -779,7 +781,8 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
       const int t = tc0 + j;
       if (EDGE && (t < 0 || t >= H)) continue;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) o.v[c] = v6[j].v[c] > kValid ? p.md - v6[j].v[c] : 0.0f;
+      for (int c = 0; c < 4; ++c)
+        o.v[c] = BLUR == kBlurRaw ? v6[j].v[c] : (v6[j].v[c] > kValid ? p.md - v6[j].v[c] : 0.0f);
       if (S.outm) store_lane<VEC>(orow, o, S.outm);
     }
     if (FULL && !EDGE && tc0 > S.tmaxN) {
@@ -1012,16 +1015,26 @@ bool fused_supported(const dfc_config& c, int H, int W) {
   if (c.multiscale || c.custom_n > 0 || (c.flags & DFC_F_EXACT_BLUR)) return false;
   if (c.dilation_shape != DFC_SHAPE_DIAMOND || c.dilation_size != 5) return false;
   if (c.closure_size != 5 || c.small_fill_size != 7 || c.large_fill_size != 31) return false;
-  if (c.blur_mode != DFC_BLUR_GAUSSIAN && c.blur_mode != DFC_BLUR_NONE) return false;
-  if (c.blur_mode == DFC_BLUR_GAUSSIAN && c.gaussian_size != 5) return false;
+  // Gaussian-5 and no blur run inside the kernel; every other blur goes
+  // through the raw mode and the blur-tail kernel
+  const bool direct = c.blur_mode == DFC_BLUR_NONE || (c.blur_mode == DFC_BLUR_GAUSSIAN && c.gaussian_size == 5);
+  if (!direct && !blur_tail_supported(c)) return false;
   if (H < 16 || W < 16) return false;
   const Layout L = layout(W);
   return L.nw <= kNW && L.smem <= 232448;
 }
 
-size_t fused_workspace_bytes(const dfc_config&, int64_t B, int, int) {
-  // [0] u64 frames needing the staged path, [8] u32 work counter, [16..) u32 umax[B]
-  return 16 + (size_t)B * 4 + 256;
+bool raw_mode(const dfc_config& c) {
+  return !(c.blur_mode == DFC_BLUR_NONE || (c.blur_mode == DFC_BLUR_GAUSSIAN && c.gaussian_size == 5));
+}
+
+size_t raw_offset(int64_t B) { return ((16 + (size_t)B * 4) + 255) & ~(size_t)255; }
+
+size_t fused_workspace_bytes(const dfc_config& c, int64_t B, int H, int W) {
+  // [0] u64 frames needing the staged path, [8] u32 work counter, [16..) u32 umax[B],
+  // then (raw mode) the stage-6 maps of one chunk of frames
+  const int64_t chunk = B < kRawChunk ? B : kRawChunk;
+  return raw_offset(B) + (raw_mode(c) ? (size_t)chunk * H * W * 4 : 0) + 256;
 }
 
 cudaError_t launch_fused(const float* in, float* out, int64_t B, int H, int W, const dfc_config& c,
@@ -1058,22 +1071,40 @@ cudaError_t launch_fused(const float* in, float* out, int64_t B, int H, int W, c
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t items = B * L.strips;
-  const int64_t slots = (int64_t)sms * L.per_sm;
-  const int grid = (int)(items < slots ? items : slots);
   const int vec = (W % 4 == 0) ? 4 : ((W % 2 == 0) ? 2 : 1);
   const bool full = c.fill_mode == DFC_FILL_FULL;
-  const bool gauss = c.blur_mode == DFC_BLUR_GAUSSIAN;
-#define DFC_DISPATCH(V)                                                      \
-  (full ? (gauss ? launch_t<V, true, DFC_BLUR_GAUSSIAN>(p, L.smem, grid, s)  \
-                 : launch_t<V, true, DFC_BLUR_NONE>(p, L.smem, grid, s))     \
-        : (gauss ? launch_t<V, false, DFC_BLUR_GAUSSIAN>(p, L.smem, grid, s) \
-                 : launch_t<V, false, DFC_BLUR_NONE>(p, L.smem, grid, s)))
-  e = vec == 4 ? DFC_DISPATCH(4) : (vec == 2 ? DFC_DISPATCH(2) : DFC_DISPATCH(1));
+  const bool raw = raw_mode(c);
+  const int blur = raw ? kBlurRaw : c.blur_mode;
+  const int64_t HW = (int64_t)H * W;
+  const int64_t chunk = raw ? (B < kRawChunk ? B : kRawChunk) : B;
+  float* tmp = raw ? reinterpret_cast<float*>(w8 + raw_offset(B)) : nullptr;
+  unsigned* umax0 = p.umax;
+  for (int64_t f0 = 0; f0 < B; f0 += chunk) {
+    const int64_t C = B - f0 < chunk ? B - f0 : chunk;
+    p.in = in + f0 * HW;
+    p.out = raw ? tmp : out + f0 * HW;
+    p.nframes = C;
+    p.status = status + f0;
+    p.iters = iters ? iters + f0 : nullptr;
+    p.umax = umax0 + f0;
+    if (f0 > 0 && (e = cudaMemsetAsync(p.work, 0, 4, s)) != cudaSuccess) return e;
+    const int64_t items = C * L.strips;
+    const int64_t slots = (int64_t)sms * L.per_sm;
+    const int grid = (int)(items < slots ? items : slots);
+#define DFC_DISPATCH(V)                                                                        \
+  (full ? (blur == DFC_BLUR_GAUSSIAN ? launch_t<V, true, DFC_BLUR_GAUSSIAN>(p, L.smem, grid, s)  \
+                                     : (blur == DFC_BLUR_NONE ? launch_t<V, true, DFC_BLUR_NONE>(p, L.smem, grid, s) \
+                                                              : launch_t<V, true, kBlurRaw>(p, L.smem, grid, s))) \
+        : (blur == DFC_BLUR_GAUSSIAN ? launch_t<V, false, DFC_BLUR_GAUSSIAN>(p, L.smem, grid, s) \
+                                     : (blur == DFC_BLUR_NONE ? launch_t<V, false, DFC_BLUR_NONE>(p, L.smem, grid, s) \
+                                                              : launch_t<V, false, kBlurRaw>(p, L.smem, grid, s))))
+    e = vec == 4 ? DFC_DISPATCH(4) : (vec == 2 ? DFC_DISPATCH(2) : DFC_DISPATCH(1));
 #undef DFC_DISPATCH
-  if (e != cudaSuccess) return e;
+    if (e != cudaSuccess) return e;
+    if (raw && (e = launch_blur_tail(tmp, out + f0 * HW, C, H, W, c, s)) != cudaSuccess) return e;
+  }
   note_launch();
-  finalize_kernel<<<(unsigned)B, 256, 0, s>>>(in, (int64_t)H * W, p.umax, status, c.max_depth);
+  finalize_kernel<<<(unsigned)B, 256, 0, s>>>(in, HW, umax0, status, c.max_depth);
   return cudaGetLastError();
 }
 

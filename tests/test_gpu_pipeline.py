@@ -290,7 +290,8 @@ def _geom_frames(h, w, n, seed):
 
 @pytest.mark.parametrize("h,w", GEOMS)
 @pytest.mark.parametrize("blur,fill", [("gaussian", "full"), ("none", "full"), ("gaussian", "partial"),
-                                       ("none", "partial")])
+                                       ("none", "partial"), ("median_bilateral", "full"), ("median", "partial"),
+                                       ("bilateral", "partial"), ("median_gaussian", "partial")])
 def test_fused_geometries_vs_oracle(P, h, w, blur, fill):
     """Frame shapes that exercise strips, W % 4 != 0, lane halos and tiny H."""
     frames = _geom_frames(h, w, 3, h * 7 + w)
@@ -322,7 +323,7 @@ def test_fused_random_sparse_frames(P):
         m = rng.random(frames[i].shape) < [0.002, 0.01, 0.03, 0.08, 0.2, 0.5][i]
         frames[i][m] = rng.uniform(0.05, 99.99, m.sum()).astype(np.float32)
     frames[2, :, 100:140] = 0  # empty column band
-    for blur in ("gaussian", "none"):
+    for blur in ("gaussian", "none", "median_bilateral", "median"):
         kw = {"blur_mode": blur, "fill_mode": "full"}
         res = P.complete_batch(frames, _pcfg(P, kw))
         got = res.dense.cpu().numpy()

@@ -91,31 +91,6 @@ dfc_config fit_to_frame(const dfc_config& c, int H, int W) {
   return o;
 }
 
-// make_kernel + kernel_offsets (kernels.py:45-78): row-major (dy,dx) list
-std::vector<int32_t> kernel_offsets(int shape, int size, bool* is_full) {
-  std::vector<int32_t> o;
-  const int r = size / 2;
-  bool full = true;
-  for (int dy = -r; dy <= r; ++dy)
-    for (int dx = -r; dx <= r; ++dx) {
-      bool on;
-      switch (shape) {
-        case DFC_SHAPE_FULL: on = true; break;
-        case DFC_SHAPE_DIAMOND: on = std::abs(dx) + std::abs(dy) <= r; break;
-        case DFC_SHAPE_CROSS: on = dx == 0 || dy == 0; break;
-        default: on = 4 * (dx * dx + dy * dy) <= size * size; break;
-      }
-      if (on) {
-        o.push_back(dy);
-        o.push_back(dx);
-      } else {
-        full = false;
-      }
-    }
-  *is_full = full;
-  return o;
-}
-
 // ---- staged pipeline -------------------------------------------------------
 
 struct StagedBufs {
@@ -157,7 +132,7 @@ StagedBufs carve_staged(void* ws, int64_t chunk, int H, int W) {
 cudaError_t dilate_any(const float* in, float* out, float* tmp, int64_t B, int H, int W, int shape, int size,
                        bool is_min, cudaStream_t s) {
   bool full;
-  auto offs = kernel_offsets(shape, size, &full);
+  auto offs = dfc::kernel_offsets(shape, size, &full);
   if (full) {
     cudaError_t e = dfc::launch_line_minmax(in, tmp, B, H, W, size / 2, is_min, 1, s);
     if (e != cudaSuccess) return e;

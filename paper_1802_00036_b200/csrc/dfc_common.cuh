@@ -4,6 +4,8 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <cstdlib>
+#include <vector>
 
 #include "dfc.h"
 
@@ -27,6 +29,32 @@ struct MinOp {
   static __device__ __forceinline__ float identity() { return 3.402823466e38f; }
   static __device__ __forceinline__ float apply(float a, float b) { return fminf(a, b); }
 };
+
+// make_kernel + kernel_offsets (kernels.py:45-78): row-major (dy,dx) list of
+// the Fig. 3 shape; *is_full when every cell of the size x size square is on
+inline std::vector<int32_t> kernel_offsets(int shape, int size, bool* is_full) {
+  std::vector<int32_t> o;
+  const int r = size / 2;
+  bool full = true;
+  for (int dy = -r; dy <= r; ++dy)
+    for (int dx = -r; dx <= r; ++dx) {
+      bool on;
+      switch (shape) {
+        case DFC_SHAPE_FULL: on = true; break;
+        case DFC_SHAPE_DIAMOND: on = std::abs(dx) + std::abs(dy) <= r; break;
+        case DFC_SHAPE_CROSS: on = dx == 0 || dy == 0; break;
+        default: on = 4 * (dx * dx + dy * dy) <= size * size; break;
+      }
+      if (on) {
+        o.push_back(dy);
+        o.push_back(dx);
+      } else {
+        full = false;
+      }
+    }
+  *is_full = full;
+  return o;
+}
 
 // process-wide count of kernels launched by libdfc (diagnostics for the bench)
 extern std::atomic<unsigned long long> g_kernel_launches;
@@ -62,6 +90,11 @@ cudaError_t launch_finalize_status(const int64_t* n_valid, uint32_t* status, int
 bool blur_tail_supported(const dfc_config& c);
 cudaError_t launch_blur_tail(const float* in, float* out, int64_t B, int H, int W, const dfc_config& c,
                              cudaStream_t s);
+
+// ---- multiscale stage 1 + 2 (multiscale.cu) -------------------------------
+bool multiscale_stage2_supported(const dfc_config& c);
+cudaError_t launch_multiscale_stage2(const float* in, float* out, int64_t B, int H, int W, const dfc_config& c,
+                                     const int32_t* const offs[3], const int n[3], unsigned* umax, cudaStream_t s);
 
 // ---- fused pipeline (fused.cu) -------------------------------------------
 struct FusedPlan;

@@ -38,6 +38,7 @@
 
 #include <climits>
 #include <cmath>
+#include <vector>
 
 #include "dfc_common.cuh"
 
@@ -52,9 +53,17 @@ constexpr int kB = 4;                  // rows per block
 constexpr int kRing = 40;              // stage-5 ring rows (39 live)
 constexpr int kRingBlocks = kRing / kB;
 constexpr int kLag = 16;               // consumer lag behind the stage-5 producer (>= 15)
-constexpr int kPLag = 9;               // stage-5 lag behind the input: 1+1+2+2+3
-constexpr int kCLag = kPLag + kLag;    // consumer rows = t0 - 25 + j
-constexpr int kKFirst = (kCLag - 1 + kB - 1) / kB;  // first consumer block (needs rows <= +15 produced)
+// Row lags (processing order).  Stage 5 trails the input by 1+1+2+2+3 = 9
+// rows (cross3, cross3, max5, min5, max7); with a precomputed stage-2 map
+// (PRE: multiscale) by 2+2+3 = 7.  The consumer trails stage 5 by kLag; its
+// first block is the one whose rows start in [-3, 0].
+template <bool PRE>
+struct Lags {
+  static constexpr int L2 = PRE ? 0 : 2;  // stage-2 lag
+  static constexpr int P = L2 + 7;        // stage-5 lag
+  static constexpr int C = P + kLag;      // consumer rows = t0 - C + j
+  static constexpr int KFirst = C / kB;
+};
 constexpr int kLF = 15;                // large fill radius
 constexpr int kStripMax = 1248;        // widest strip handled by one CTA
 constexpr float kFMax = 3.402823466e38f;
@@ -326,7 +335,9 @@ __device__ void item_geometry(int s, const Params& p, int warp, Geo& g) {
 // ---------------------------------------------------------------------------
 // Phase 1: first valid stage-4 row per column, bit-packed morphology
 // ---------------------------------------------------------------------------
-template <int VEC>
+// bit i of w[c]: (inverted) validity of row y0 + i; PRE: the frame is the
+// stage-2 map in the inverted encoding already
+template <int VEC, bool PRE>
 __device__ __forceinline__ void load_bits(const float* frame, int H, int W, int x0, int y0, float md, uint32_t w[4],
                                           unsigned& umax) {
 #pragma unroll
@@ -347,9 +358,13 @@ __device__ __forceinline__ void load_bits(const float* frame, int H, int W, int 
     for (int i = 0; i < 16; ++i)
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        umax = max(umax, __float_as_uint(v[i].v[c]));
-        const float inv = v[i].v[c] > kValid ? md - v[i].v[c] : 0.0f;
-        w[c] |= (uint32_t)(inv > kValid) << (16 * h + i);
+        if constexpr (PRE) {
+          w[c] |= (uint32_t)(v[i].v[c] > kValid) << (16 * h + i);
+        } else {
+          umax = max(umax, __float_as_uint(v[i].v[c]));
+          const float inv = v[i].v[c] > kValid ? md - v[i].v[c] : 0.0f;
+          w[c] |= (uint32_t)(inv > kValid) << (16 * h + i);
+        }
       }
   }
 }
@@ -385,13 +400,13 @@ __device__ __forceinline__ void hcomb(const uint64_t in[4], uint64_t out[4]) {
   }
 }
 
-template <int VEC>
+template <int VEC, bool PRE>
 __device__ __forceinline__ void phase1(const float* frame, const Params& p, int x0, bool needed, unsigned incol,
                                        int T0[4], unsigned& umax) {
   const int H = p.H, W = p.W;
   uint32_t prv[4] = {0, 0, 0, 0}, cur[4], nxt[4];
-  load_bits<VEC>(frame, H, W, x0, 0, p.md, cur, umax);
-  load_bits<VEC>(frame, H, W, x0, 32, p.md, nxt, umax);
+  load_bits<VEC, PRE>(frame, H, W, x0, 0, p.md, cur, umax);
+  load_bits<VEC, PRE>(frame, H, W, x0, 32, p.md, nxt, umax);
   int r0[4] = {-1, -1, -1, -1};
   uint64_t cm[4];
 #pragma unroll
@@ -403,9 +418,9 @@ __device__ __forceinline__ void phase1(const float* frame, const Params& p, int 
 #pragma unroll
     for (int c = 0; c < 4; ++c)
       X[c] = ((uint64_t)(prv[c] >> 16) | ((uint64_t)cur[c] << 16) | ((uint64_t)nxt[c] << 48)) & cm[c];
-    // D_shape = cross3 o cross3 (5x5 diamond)
+    // D_shape = cross3 o cross3 (5x5 diamond); PRE: the stage-2 validity is loaded
 #pragma unroll
-    for (int it = 0; it < 2; ++it) {
+    for (int it = 0; it < (PRE ? 0 : 2); ++it) {
       hcomb<1, false>(X, A);
 #pragma unroll
       for (int c = 0; c < 4; ++c) Bq[c] = (vdil(X[c], 1) | A[c]) & inrow & cm[c];
@@ -437,7 +452,7 @@ __device__ __forceinline__ void phase1(const float* frame, const Params& p, int 
       prv[c] = cur[c];
       cur[c] = nxt[c];
     }
-    load_bits<VEC>(frame, H, W, x0, 32 * (b + 2), p.md, nxt, umax);
+    load_bits<VEC, PRE>(frame, H, W, x0, 32 * (b + 2), p.md, nxt, umax);
   }
 #pragma unroll
   for (int c = 0; c < 4; ++c) T0[c] = r0[c] >= 0 ? (H - 1 - r0[c]) : INT_MAX;
@@ -451,6 +466,7 @@ __device__ __forceinline__ void phase1(const float* frame, const Params& p, int 
 // Stage-5 values are >= 0, so their float bit patterns order like the values
 // and one redux.max combines the lanes.
 // ---------------------------------------------------------------------------
+template <int PLAG>
 __device__ __forceinline__ float lf_one(const float* __restrict__ ring, int ringw, int p0, int p1, int H, int lane,
                                         int x, int row) {
   const int col = x - kLF + lane;
@@ -458,7 +474,7 @@ __device__ __forceinline__ float lf_one(const float* __restrict__ ring, int ring
   if (lane < 2 * kLF + 1 && col >= p0 && col < p1) {
     const float* rc = ring + (col - p0);
     const int r0 = max(row - kLF, 0), r1 = min(row + kLF, H - 1);
-    int slot = (r0 + kPLag) % kRing;
+    int slot = (r0 + PLAG) % kRing;
 #pragma unroll 8
     for (int r = r0; r <= r1; ++r) {
       m = max(m, __float_as_uint(rc[slot * ringw]));
@@ -497,11 +513,13 @@ struct State {
   int srcL, srcR, compR;  // replicate sources for out-of-frame columns
 };
 
-template <int VEC, bool FULL, int BLUR, bool EDGE>
+template <int VEC, bool FULL, int BLUR, bool PRE, bool EDGE>
 __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
+  using LG = Lags<PRE>;
   const int H = p.H, W = p.W;
   const int t0 = kB * k;
-  const int tp = t0 - kPLag;
+  const int tp = t0 - LG::P;
+  constexpr int L2 = LG::L2;
   // ======================= producer =======================
   if (FULL && !S.skip && tp > S.tmax) S.skip = true;
   F4 f[kB];
@@ -511,25 +529,38 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
 #pragma unroll
     for (int j = 0; j < kB; ++j) {
       a[j] = lds4(S.stg + j * 512);
+      if constexpr (!PRE) {
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const float v = a[j].v[c];
-        S.umax = max(S.umax, __float_as_uint(v));
-        a[j].v[c] = v > kValid ? p.md - v : 0.0f;
+        for (int c = 0; c < 4; ++c) {
+          const float v = a[j].v[c];
+          S.umax = max(S.umax, __float_as_uint(v));
+          a[j].v[c] = v > kValid ? p.md - v : 0.0f;
+        }
       }
     }
     // stage the next block; stops once its stage-5 rows lie above every r0.
-    // umax depends on every staged value: the shared reads are complete
-    // before the slot is overwritten.
-    asm volatile("" ::"r"(S.umax));
-    if (!FULL || (t0 + kB - kPLag <= S.tmax)) {
+    // The values read above are materialised first: the shared reads are
+    // complete before the slot is overwritten.
+    if constexpr (PRE) {
+#pragma unroll
+      for (int j = 0; j < kB; ++j)
+        asm volatile("" ::"f"(a[j].v[0]), "f"(a[j].v[1]), "f"(a[j].v[2]), "f"(a[j].v[3]));
+    } else {
+      asm volatile("" ::"r"(S.umax));
+    }
+    if (!FULL || (t0 + kB - LG::P <= S.tmax)) {
       const float* q = S.lrow;
 #pragma unroll
       for (int j = 0; j < kB; ++j, q -= W)
         stage_lane<VEC>(S.stg + j * 512, q, p.in, !EDGE || t0 + kB + j < H, S.full, S.incol);
       cp_async_commit();
     }
-    // --- cross3 #1 (rows t0-1+j) ---
+    // --- stage 2: cross3 o cross3 = 5x5 diamond (rows t0-2+j); PRE: the staged rows ---
+    F4 d2[kB];
+    if constexpr (PRE) {
+#pragma unroll
+      for (int j = 0; j < kB; ++j) d2[j] = a[j];  // rows >= H and out-of-frame columns were staged as 0
+    } else {
     F4 d1[kB];
     {
       const F4 in[kB + 2] = {S.c1[0], S.c1[1], a[0], a[1], a[2], a[3]};
@@ -548,7 +579,6 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
       }
     }
     // --- cross3 #2 (rows t0-2+j) ---
-    F4 d2[kB];
     {
       const F4 in[kB + 2] = {S.c2[0], S.c2[1], d1[0], d1[1], d1[2], d1[3]};
 #pragma unroll
@@ -565,7 +595,8 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
         if (S.woob) fix_oob(d2[j], S.oob, 0.f);
       }
     }
-    // --- close: max5 (rows t0-4+j) ---
+    }
+    // --- close: max5 (rows t0-L2-2+j) ---
     F4 m5[kB];
     {
       const F4 in[kB + 4] = {S.c3[0], S.c3[1], S.c3[2], S.c3[3], d2[0], d2[1], d2[2], d2[3]};
@@ -577,11 +608,11 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
       for (int i = 0; i < 4; ++i) S.c3[i] = d2[i];
 #pragma unroll
       for (int j = 0; j < kB; ++j) {
-        if (EDGE && (t0 - 4 + j < 0 || t0 - 4 + j >= H)) set_row(m5[j], kFMax);
+        if (EDGE && (t0 - L2 - 2 + j < 0 || t0 - L2 - 2 + j >= H)) set_row(m5[j], kFMax);
         if (S.woob) fix_oob(m5[j], S.oob, kFMax);
       }
     }
-    // --- close: min5 (rows t0-6+j) ---
+    // --- close: min5 (rows t0-L2-4+j) ---
     F4 cl[kB];
     {
       const F4 in[kB + 4] = {S.c4[0], S.c4[1], S.c4[2], S.c4[3], m5[0], m5[1], m5[2], m5[3]};
@@ -593,11 +624,11 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
       for (int i = 0; i < 4; ++i) S.c4[i] = m5[i];
 #pragma unroll
       for (int j = 0; j < kB; ++j) {
-        if (EDGE && (t0 - 6 + j < 0 || t0 - 6 + j >= H)) set_row(cl[j], 0.f);
+        if (EDGE && (t0 - L2 - 4 + j < 0 || t0 - L2 - 4 + j >= H)) set_row(cl[j], 0.f);
         if (S.woob) fix_oob(cl[j], S.oob, 0.f);
       }
     }
-    // --- small fill: masked max7 (rows t0-9+j) ---
+    // --- small fill: masked max7 (rows t0-L2-7+j = tp+j) ---
     {
       const F4 in[kB + 6] = {S.c5[0], S.c5[1], S.c5[2], S.c5[3], S.c5[4], S.c5[5], cl[0], cl[1], cl[2], cl[3]};
       F4 vv[kB];
@@ -634,7 +665,7 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
       for (int c = 0; c < 4; ++c) f[j].v[c] = S.top[c];
   }
   S.lrow -= kB * W;
-  // --- ring store: ring slot of row t is (t + 9) mod 40, so this block is slots 4*(k mod 10) + j ---
+  // --- ring store: ring slot of row t is (t + P) mod 40, so this block is slots 4*(k mod 10) + j ---
   if (S.own) {
     float* w = S.wring + (k % kRingBlocks) * kB * S.ringw;
 #pragma unroll
@@ -644,8 +675,8 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
   }
   __syncthreads();
   // ======================= consumer =======================
-  const int tc0 = t0 - kCLag;
-  if (k < kKFirst) return;
+  const int tc0 = t0 - LG::C;
+  if (k < LG::KFirst) return;
   float* orow = S.orow;  // output row of processing row tc0 - 2
   S.orow -= kB * W;
   if (FULL && S.fast) {
@@ -668,7 +699,7 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
       const float* rr = r + j * S.ringw;
       if (EDGE) {
         const int t = min(max(tc0 + j, 0), H - 1);
-        rr = S.rring + ((t + kPLag) % kRing) * S.ringw;
+        rr = S.rring + ((t + LG::P) % kRing) * S.ringw;
       }
       const float4 q = *reinterpret_cast<const float4*>(rr);
       v6[j].v[0] = q.x, v6[j].v[1] = q.y, v6[j].v[2] = q.z, v6[j].v[3] = q.w;
@@ -697,7 +728,7 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
           const int b = __ffs(pe) - 1;
           pe &= pe - 1;
           const int row = EDGE ? min(max(tc0 + (b >> 2), 0), H - 1) : tc0 + (b >> 2);
-          const float r = lf_one(S.ring, S.ringw, S.p0, S.p1, H, S.lane, S.L + 4 * src + (b & 3), row);
+          const float r = lf_one<LG::P>(S.ring, S.ringw, S.p0, S.p1, H, S.lane, S.L + 4 * src + (b & 3), row);
           if (S.lane == src) {
 #pragma unroll
             for (int j = 0; j < kB; ++j)
@@ -736,7 +767,7 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
         h[j].v[2 * hp + 1] = a.y;
       }
     }
-    if (EDGE && k == kKFirst) {  // rows above row 0 replicate it (tc0 = -1: h[0] is row 0)
+    if (EDGE && k == LG::KFirst) {  // rows above row 0 replicate it (tc0 in [-3, 0]: h[0] is row 0)
 #pragma unroll
       for (int i = 0; i < 4; ++i) S.gc[i] = h[0];
     }
@@ -795,8 +826,9 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
 // ---------------------------------------------------------------------------
 // the fused kernel
 // ---------------------------------------------------------------------------
-template <int VEC, bool FULL, int BLUR>
+template <int VEC, bool FULL, int BLUR, bool PRE>
 __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constant__ Params p) {
+  using LG = Lags<PRE>;
   extern __shared__ __align__(16) float smem[];
   __shared__ unsigned s_item;
   const int lane = threadIdx.x & 31;
@@ -860,7 +892,7 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
     for (int c = 0; c < 4; ++c) S.T0[c] = INT_MAX, S.top[c] = 0.f;
     S.tmax = S.tmin = INT_MAX;
     if (FULL) {
-      phase1<VEC>(src, p, S.x0, (S.own | needm) != 0, incol, S.T0, S.umax);
+      phase1<VEC, PRE>(src, p, S.x0, (S.own | needm) != 0, incol, S.T0, S.umax);
       int mx = INT_MIN, mn = INT_MAX, mxn = INT_MIN;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -889,23 +921,23 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
       stage_lane<VEC>(S.stg + j * 512, src + (int64_t)(H - 1 - j) * W + S.x0, p.in, j < H, S.full, incol);
     cp_async_commit();
     S.lrow = src + (int64_t)(H - 1 - kB) * W + S.x0;
-    S.orow = dst + (int64_t)(H - 1 - (kB * kKFirst - kCLag - 2)) * W + S.x0;
+    S.orow = dst + (int64_t)(H - 1 - (kB * LG::KFirst - LG::C - 2)) * W + S.x0;
 
     // iterations with every row inside the frame run the lean body
-    const int K = (H + kCLag + 2) / kB + 1;
-    const int kLo = (kCLag + 2 + kB - 1) / kB;  // tc0 - 2 >= 0 and tp >= 0
+    const int K = (H + LG::C + 2) / kB + 1;
+    const int kLo = (LG::C + 2 + kB - 1) / kB;  // tc0 - 2 >= 0 and tp >= 0
     const int kHi = (H - 2 * kB) / kB;           // t0 + 7 <= H - 1 and tc0 + 3 <= H - 1
     int k = 0;
-    for (; k < min(kLo, K); ++k) iterate<VEC, FULL, BLUR, true>(p, S, k);
-    for (; k <= kHi; ++k) iterate<VEC, FULL, BLUR, false>(p, S, k);
-    for (; k < K; ++k) iterate<VEC, FULL, BLUR, true>(p, S, k);
+    for (; k < min(kLo, K); ++k) iterate<VEC, FULL, BLUR, PRE, true>(p, S, k);
+    for (; k <= kHi; ++k) iterate<VEC, FULL, BLUR, PRE, false>(p, S, k);
+    for (; k < K; ++k) iterate<VEC, FULL, BLUR, PRE, true>(p, S, k);
 
     // ---------------- per-frame flags ----------------
     const unsigned um = __reduce_max_sync(kFull, S.umax);
     const bool he = __any_sync(kFull, S.had_empty);
     const bool se = __any_sync(kFull, S.still_empty);
     if (lane == 0) {
-      atomicMax(p.umax + frame, um);
+      if (!PRE) atomicMax(p.umax + frame, um);  // PRE: multiscale.cu records it
       if (FULL && he && p.iters) atomicOr(p.iters + frame, 1);
       if (FULL && se) {
         atomicOr(p.status + frame, kNeedsStaged);
@@ -999,9 +1031,9 @@ Layout layout_for(int W, int strips) {
 // strip halos and phase 1 are paid twice).
 Layout layout(int W) { return layout_for(W, W <= kStripMax ? 1 : (W + 1023) / 1024); }
 
-template <int VEC, bool FULL, int BLUR>
+template <int VEC, bool FULL, int BLUR, bool PRE>
 cudaError_t launch_t(const Params& p, size_t smem, int grid, cudaStream_t s) {
-  auto k = fused_kernel<VEC, FULL, BLUR>;
+  auto k = fused_kernel<VEC, FULL, BLUR, PRE>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   note_launch();
@@ -1009,11 +1041,33 @@ cudaError_t launch_t(const Params& p, size_t smem, int grid, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+template <int VEC, bool FULL>
+cudaError_t dispatch_blur(int blur, bool pre, const Params& p, size_t smem, int grid, cudaStream_t s) {
+  if (pre) {
+    if (blur == DFC_BLUR_GAUSSIAN) return launch_t<VEC, FULL, DFC_BLUR_GAUSSIAN, true>(p, smem, grid, s);
+    if (blur == DFC_BLUR_NONE) return launch_t<VEC, FULL, DFC_BLUR_NONE, true>(p, smem, grid, s);
+    return launch_t<VEC, FULL, kBlurRaw, true>(p, smem, grid, s);
+  }
+  if (blur == DFC_BLUR_GAUSSIAN) return launch_t<VEC, FULL, DFC_BLUR_GAUSSIAN, false>(p, smem, grid, s);
+  if (blur == DFC_BLUR_NONE) return launch_t<VEC, FULL, DFC_BLUR_NONE, false>(p, smem, grid, s);
+  return launch_t<VEC, FULL, kBlurRaw, false>(p, smem, grid, s);
+}
+
+cudaError_t dispatch(int vec, bool full, int blur, bool pre, const Params& p, size_t smem, int grid, cudaStream_t s) {
+  if (vec == 4) return full ? dispatch_blur<4, true>(blur, pre, p, smem, grid, s)
+                            : dispatch_blur<4, false>(blur, pre, p, smem, grid, s);
+  if (vec == 2) return full ? dispatch_blur<2, true>(blur, pre, p, smem, grid, s)
+                            : dispatch_blur<2, false>(blur, pre, p, smem, grid, s);
+  return full ? dispatch_blur<1, true>(blur, pre, p, smem, grid, s) : dispatch_blur<1, false>(blur, pre, p, smem, grid, s);
+}
+
 }  // namespace
 
 bool fused_supported(const dfc_config& c, int H, int W) {
-  if (c.multiscale || c.custom_n > 0 || (c.flags & DFC_F_EXACT_BLUR)) return false;
-  if (c.dilation_shape != DFC_SHAPE_DIAMOND || c.dilation_size != 5) return false;
+  if (c.custom_n > 0 || (c.flags & DFC_F_EXACT_BLUR)) return false;
+  if (c.multiscale ? !multiscale_stage2_supported(c)
+                   : (c.dilation_shape != DFC_SHAPE_DIAMOND || c.dilation_size != 5))
+    return false;
   if (c.closure_size != 5 || c.small_fill_size != 7 || c.large_fill_size != 31) return false;
   // Gaussian-5 and no blur run inside the kernel; every other blur goes
   // through the raw mode and the blur-tail kernel
@@ -1030,11 +1084,20 @@ bool raw_mode(const dfc_config& c) {
 
 size_t raw_offset(int64_t B) { return ((16 + (size_t)B * 4) + 255) & ~(size_t)255; }
 
+// frames per fused round when intermediate maps go through the workspace:
+// two CTA waves on a 148-SM B200
+int64_t round_frames(const dfc_config& c, int64_t B, int W) {
+  if (!raw_mode(c) && !c.multiscale) return B;
+  const int64_t ch = (kRawChunk + layout(W).strips - 1) / layout(W).strips;
+  return B < ch ? B : ch;
+}
+
 size_t fused_workspace_bytes(const dfc_config& c, int64_t B, int H, int W) {
   // [0] u64 frames needing the staged path, [8] u32 work counter, [16..) u32 umax[B],
-  // then (raw mode) the stage-6 maps of one chunk of frames
-  const int64_t chunk = B < kRawChunk ? B : kRawChunk;
-  return raw_offset(B) + (raw_mode(c) ? (size_t)chunk * H * W * 4 : 0) + 256;
+  // then one round of stage-6 maps (raw mode) and of stage-2 maps (multiscale)
+  const size_t map = (size_t)round_frames(c, B, W) * H * W * 4;
+  const size_t a = (map + 255) & ~(size_t)255;
+  return raw_offset(B) + (raw_mode(c) ? a : 0) + (c.multiscale ? a : 0) + 256;
 }
 
 cudaError_t launch_fused(const float* in, float* out, int64_t B, int H, int W, const dfc_config& c,
@@ -1076,12 +1139,30 @@ cudaError_t launch_fused(const float* in, float* out, int64_t B, int H, int W, c
   const bool raw = raw_mode(c);
   const int blur = raw ? kBlurRaw : c.blur_mode;
   const int64_t HW = (int64_t)H * W;
-  const int64_t chunk = raw ? (B < kRawChunk ? B : kRawChunk) : B;
+  const bool pre = c.multiscale != 0;
+  const int64_t chunk = round_frames(c, B, W);
+  const size_t map = (((size_t)chunk * HW * 4) + 255) & ~(size_t)255;
   float* tmp = raw ? reinterpret_cast<float*>(w8 + raw_offset(B)) : nullptr;
+  float* s2 = pre ? reinterpret_cast<float*>(w8 + raw_offset(B) + (raw ? map : 0)) : nullptr;
   unsigned* umax0 = p.umax;
+  std::vector<int32_t> offs[3];
+  const int32_t* op[3];
+  int on[3];
+  if (pre) {
+    const int shp[3] = {c.near_shape, c.med_shape, c.far_shape};
+    const int siz[3] = {c.near_size, c.med_size, c.far_size};
+    for (int k = 0; k < 3; ++k) {
+      bool full;
+      offs[k] = kernel_offsets(shp[k], siz[k], &full);
+      op[k] = offs[k].data();
+      on[k] = (int)offs[k].size() / 2;
+    }
+  }
   for (int64_t f0 = 0; f0 < B; f0 += chunk) {
     const int64_t C = B - f0 < chunk ? B - f0 : chunk;
-    p.in = in + f0 * HW;
+    if (pre && (e = launch_multiscale_stage2(in + f0 * HW, s2, C, H, W, c, op, on, umax0 + f0, s)) != cudaSuccess)
+      return e;
+    p.in = pre ? s2 : in + f0 * HW;
     p.out = raw ? tmp : out + f0 * HW;
     p.nframes = C;
     p.status = status + f0;
@@ -1091,15 +1172,7 @@ cudaError_t launch_fused(const float* in, float* out, int64_t B, int H, int W, c
     const int64_t items = C * L.strips;
     const int64_t slots = (int64_t)sms * L.per_sm;
     const int grid = (int)(items < slots ? items : slots);
-#define DFC_DISPATCH(V)                                                                        \
-  (full ? (blur == DFC_BLUR_GAUSSIAN ? launch_t<V, true, DFC_BLUR_GAUSSIAN>(p, L.smem, grid, s)  \
-                                     : (blur == DFC_BLUR_NONE ? launch_t<V, true, DFC_BLUR_NONE>(p, L.smem, grid, s) \
-                                                              : launch_t<V, true, kBlurRaw>(p, L.smem, grid, s))) \
-        : (blur == DFC_BLUR_GAUSSIAN ? launch_t<V, false, DFC_BLUR_GAUSSIAN>(p, L.smem, grid, s) \
-                                     : (blur == DFC_BLUR_NONE ? launch_t<V, false, DFC_BLUR_NONE>(p, L.smem, grid, s) \
-                                                              : launch_t<V, false, kBlurRaw>(p, L.smem, grid, s))))
-    e = vec == 4 ? DFC_DISPATCH(4) : (vec == 2 ? DFC_DISPATCH(2) : DFC_DISPATCH(1));
-#undef DFC_DISPATCH
+    e = dispatch(vec, full, blur, pre, p, L.smem, grid, s);
     if (e != cudaSuccess) return e;
     if (raw && (e = launch_blur_tail(tmp, out + f0 * HW, C, H, W, c, s)) != cudaSuccess) return e;
   }

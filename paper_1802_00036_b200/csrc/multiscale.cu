@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "dfc_common.cuh"
+#include "lane_ops.cuh"
 
 namespace dfc {
 namespace {
@@ -77,7 +78,136 @@ __global__ void __launch_bounds__(kThreads) ms_stage2_kernel(const float* __rest
   if (threadIdx.x == 0) atomicMax(umax + b, s_umax);
 }
 
+// ---------------------------------------------------------------------------
+// Streaming variant for the default bin kernels (near FULL7, medium DIAMOND7,
+// far DIAMOND5).  Each warp owns 120 columns (lanes 1..30 of 32 x 4 columns;
+// one lane of halo per side covers the radius 3) and walks the frame top-down
+// in 4-row blocks, warps independent.  FULL7 = vertical max7 then horizontal
+// max7; DIAMOND(2r+1) = cross3 applied r times.  Out-of-frame rows and columns
+// are zero between the stages (max identity for maps >= 0): for these
+// rectangle-convex shapes the dilation clipped to the frame equals the
+// reference's replicate border.  Outputs trail the input
+// by 3 rows.
+// ---------------------------------------------------------------------------
+constexpr int kMsOwn = 120;
+constexpr int kMsWarps = 4;
+
+struct MsFastParams {
+  float md, edge_near, edge_far;
+};
+
+__device__ __forceinline__ F4 cross3(const F4& up, const F4& mid, const F4& dn) {
+  const Ext<1> e = ext_row<1>(mid);
+  F4 o;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) o.v[c] = fmx3(fmx3(up.v[c], mid.v[c], dn.v[c]), e.e[c], e.e[c + 2]);
+  return o;
+}
+
+// one cross3 stage over a 4-row block with 2 carried rows; zeroes rows outside
+// [0, H) (row of output j: t0 - lag + j) and out-of-frame columns
+__device__ __forceinline__ void cross3_block(F4 carry[2], const F4 in4[kB], F4 out[kB], int row0, int H,
+                                             unsigned oob, bool edge_rows) {
+  const F4 in[kB + 2] = {carry[0], carry[1], in4[0], in4[1], in4[2], in4[3]};
+#pragma unroll
+  for (int j = 0; j < kB; ++j) {
+    out[j] = cross3(in[j], in[j + 1], in[j + 2]);
+    if (edge_rows && (row0 + j < 0 || row0 + j >= H)) set_row(out[j], 0.f);
+    fix_oob(out[j], oob, 0.f);
+  }
+  carry[0] = in4[2];
+  carry[1] = in4[3];
+}
+
+template <int VEC>
+__global__ void __launch_bounds__(kMsWarps * 32) ms_fast_kernel(const float* __restrict__ in, float* __restrict__ out,
+                                                                int H, int W, unsigned* __restrict__ umax,
+                                                                const __grid_constant__ MsFastParams p) {
+  const int lane = threadIdx.x & 31;
+  const int S0 = (blockIdx.x * kMsWarps + (threadIdx.x >> 5)) * kMsOwn;
+  if (S0 >= W) return;  // whole warp
+  const int64_t b = blockIdx.y;
+  const float* src = in + b * (int64_t)H * W;
+  float* dst = out + b * (int64_t)H * W;
+  const int x0 = S0 - 4 + 4 * lane;
+  unsigned oob = 0, own = 0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int x = x0 + c;
+    oob |= (unsigned)(x < 0 || x >= W) << c;
+    own |= (unsigned)(lane >= 1 && lane <= 30 && x < W) << c;
+  }
+  F4 nc[6], m1[2], m2[2], m3[2], f1[2], f2[2], fd;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) set_row(nc[i], 0.f);
+#pragma unroll
+  for (int i = 0; i < 2; ++i) set_row(m1[i], 0.f), set_row(m2[i], 0.f), set_row(m3[i], 0.f), set_row(f1[i], 0.f),
+      set_row(f2[i], 0.f);
+  set_row(fd, 0.f);
+  unsigned um = 0;
+  for (int t0 = 0; t0 < H + 3; t0 += kB) {
+    const bool edge_rows = t0 < 3 || t0 + kB > H;
+    F4 nv[kB], mv[kB], fv[kB];
+#pragma unroll
+    for (int j = 0; j < kB; ++j) {
+      F4 d;
+      if (t0 + j < H)
+        d = load4<VEC, true>(src + (int64_t)(t0 + j) * W, x0, W);
+      else
+        set_row(d, 0.f);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float v = d.v[c];
+        um = max(um, __float_as_uint(v));
+        const float inv = v > kValid ? p.md - v : 0.0f;  // depth_core.invert
+        nv[j].v[c] = v <= p.edge_near ? inv : 0.0f;
+        mv[j].v[c] = (v > p.edge_near && v <= p.edge_far) ? inv : 0.0f;
+        fv[j].v[c] = v > p.edge_far ? inv : 0.0f;
+      }
+    }
+    // near: FULL7 box (rows t0-3+j)
+    F4 nb[kB];
+    {
+      const F4 col[kB + 6] = {nc[0], nc[1], nc[2], nc[3], nc[4], nc[5], nv[0], nv[1], nv[2], nv[3]};
+      F4 vv[kB];
+      vwin3<OpMax>(col, vv);
+#pragma unroll
+      for (int j = 0; j < kB; ++j) nb[j] = hwin3<OpMax>(ext_row<3>(vv[j]));
+      nc[0] = nc[4], nc[1] = nc[5];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) nc[i + 2] = nv[i];
+    }
+    // medium: DIAMOND7 = cross3^3 (rows t0-1+j, t0-2+j, t0-3+j)
+    F4 a1[kB], a2[kB], a3[kB];
+    cross3_block(m1, mv, a1, t0 - 1, H, oob, edge_rows);
+    cross3_block(m2, a1, a2, t0 - 2, H, oob, edge_rows);
+    cross3_block(m3, a2, a3, t0 - 3, H, oob, edge_rows);
+    // far: DIAMOND5 = cross3^2 (rows t0-2+j), delayed one row
+    F4 b1[kB], b2[kB];
+    cross3_block(f1, fv, b1, t0 - 1, H, oob, edge_rows);
+    cross3_block(f2, b1, b2, t0 - 2, H, oob, edge_rows);
+    const F4 fr[kB] = {fd, b2[0], b2[1], b2[2]};
+    fd = b2[3];
+#pragma unroll
+    for (int j = 0; j < kB; ++j) {
+      const int y = t0 - 3 + j;
+      if (y < 0 || y >= H) continue;
+      F4 o;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) o.v[c] = fmx3(nb[j].v[c], a3[j].v[c], fr[j].v[c]);
+      store4<VEC>(dst + (int64_t)y * W, x0, o, own);
+    }
+  }
+  um = __reduce_max_sync(kFull, um);
+  if (lane == 0) atomicMax(umax + b, um);
+}
+
 }  // namespace
+
+bool multiscale_fast_kernels(const dfc_config& c) {
+  return c.near_shape == DFC_SHAPE_FULL && c.near_size == 7 && c.med_shape == DFC_SHAPE_DIAMOND && c.med_size == 7 &&
+         c.far_shape == DFC_SHAPE_DIAMOND && c.far_size == 5;
+}
 
 // kernel_offsets (capi.cu) for the three bins; false if a bin is wider than 7
 bool multiscale_stage2_supported(const dfc_config& c) {
@@ -87,6 +217,18 @@ bool multiscale_stage2_supported(const dfc_config& c) {
 
 cudaError_t launch_multiscale_stage2(const float* in, float* out, int64_t B, int H, int W, const dfc_config& c,
                                      const int32_t* const offs[3], const int n[3], unsigned* umax, cudaStream_t s) {
+  if (multiscale_fast_kernels(c)) {
+    MsFastParams q{c.max_depth, c.bin_edge_near, c.bin_edge_far};
+    const dim3 grid((unsigned)((W + kMsOwn * kMsWarps - 1) / (kMsOwn * kMsWarps)), (unsigned)B);
+    note_launch();
+    if (W % 4 == 0)
+      ms_fast_kernel<4><<<grid, kMsWarps * 32, 0, s>>>(in, out, H, W, umax, q);
+    else if (W % 2 == 0)
+      ms_fast_kernel<2><<<grid, kMsWarps * 32, 0, s>>>(in, out, H, W, umax, q);
+    else
+      ms_fast_kernel<1><<<grid, kMsWarps * 32, 0, s>>>(in, out, H, W, umax, q);
+    return cudaGetLastError();
+  }
   BinParams p{};
   p.md = c.max_depth;
   p.edge_near = c.bin_edge_near;

@@ -331,3 +331,36 @@ def test_fused_random_sparse_frames(P):
             ref, info = O.complete_with_stats(frames[i], _ocfg(kw))
             _cmp(got[i], ref, blur)
             assert int(res.iterations[i]) == info["large_fill_iterations"]
+
+
+MS_DEFAULT = ((15.0, 30.0), (O.KernelShape.FULL, 7), (O.KernelShape.DIAMOND, 7), (O.KernelShape.DIAMOND, 5))
+
+
+@pytest.mark.parametrize("h,w", GEOMS)
+@pytest.mark.parametrize("blur,fill", [("none", "full"), ("median_bilateral", "full"), ("median", "partial")])
+def test_multiscale_geometries_vs_oracle(P, h, w, blur, fill):
+    """fill_in_multiscale (default bin kernels: streaming stage-2 kernel) on odd shapes, vs the composed oracle."""
+    frames = _geom_frames(h, w, 3, h * 5 + w + 1)
+    kw = {"blur_mode": blur, "fill_mode": fill}
+    res = P.complete_batch(frames, _pcfg(P, kw), multiscale=P.MultiscaleConfig())
+    got = res.dense.cpu().numpy()
+    for i in range(frames.shape[0]):
+        ref, info = O.complete_with_stats(frames[i], O.OracleConfig(**{**_ocfg(kw).__dict__, "multiscale": MS_DEFAULT}))
+        _cmp(got[i], ref, blur)
+        assert int(res.iterations[i]) == info["large_fill_iterations"]
+
+
+@pytest.mark.parametrize("kernels", [((O.KernelShape.CROSS, 5), (O.KernelShape.CIRCLE, 7), (O.KernelShape.FULL, 3)),
+                                     ((O.KernelShape.DIAMOND, 3), (O.KernelShape.FULL, 5), (O.KernelShape.CIRCLE, 5))])
+def test_multiscale_other_kernels_vs_oracle(P, kernels):
+    """Non-default bin kernels take the generic offsets stage-2 kernel."""
+    frames = synth.make_batch(2, 300, 3)
+    kw = {"blur_mode": "none", "fill_mode": "full"}
+    ms = P.MultiscaleConfig(near=(P.KernelShape(kernels[0][0].value), kernels[0][1]),
+                            medium=(P.KernelShape(kernels[1][0].value), kernels[1][1]),
+                            far=(P.KernelShape(kernels[2][0].value), kernels[2][1]))
+    res = P.complete_batch(frames, _pcfg(P, kw), multiscale=ms)
+    got = res.dense.cpu().numpy()
+    for i in range(frames.shape[0]):
+        ref = O.complete(frames[i], O.OracleConfig(**{**_ocfg(kw).__dict__, "multiscale": ((15.0, 30.0), *kernels)}))
+        _cmp(got[i], ref, "none")

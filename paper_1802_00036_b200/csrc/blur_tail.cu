@@ -13,7 +13,7 @@
 //
 // The median is exact (selection network, bit-identical to the reference's
 // median_network).  The Gaussian is fp32 centre-relative c + sum w_i w_j (q - c) and the
-// bilateral fp32 centre-relative c + sum w (q - c) / sum w with exp2; both are
+// bilateral fp32 centre-relative c + sum w (q - c) / sum w with ex2.approx; both are
 // within the 1e-4 m bar of the float64 reference (tests/test_gpu_pipeline.py).
 // The exact float64 blurs (DFC_F_EXACT_BLUR) stay on the staged op kernels.
 #include <cuda_runtime.h>
@@ -44,6 +44,12 @@ struct TailParams {
     a = lo_;                       \
     b = hi_;                       \
   } while (0)
+
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 template <int MR>
 __device__ __forceinline__ float median_at(const float* __restrict__ t, int stride) {
@@ -96,37 +102,58 @@ __global__ void __launch_bounds__(kThreads) blur_tail_kernel(const float* __rest
   }
   __syncthreads();
 
-  // stage-7b: Gaussian / bilateral, re-impose, invert back
-  for (int i = threadIdx.x; i < kTX * kTY; i += kThreads) {
-    const int oy = i / kTX, ox = i - oy * kTX;
+  // stage-7b: Gaussian / bilateral, re-impose, invert back -- two horizontally
+  // adjacent outputs per thread in packed fp32x2 (FADD2 / FMUL2 / FFMA2)
+  for (int i = threadIdx.x; i < kTX * kTY / 2; i += kThreads) {
+    const int oy = i / (kTX / 2), ox = 2 * (i - oy * (kTX / 2));
     const int gy = y0 + oy, gx = x0 + ox;
     if (gy >= H || gx >= W) continue;
-    const float* m = sM + oy * MW + ox;  // window top-left (radius PR)
-    const float c = m[PR * MW + PR];
-    float r = c;
+    const float* m = sM + oy * MW + ox;  // window top-left of the first output (radius PR)
+    const float2 c = make_float2(m[PR * MW + PR], m[PR * MW + PR + 1]);
+    float2 r = c;
     if constexpr (POST == kPostGauss) {
       // centre-relative: constant neighbourhoods come out exactly constant
-      float a = 0.0f;
-#pragma unroll
-      for (int dy = 0; dy <= 2 * PR; ++dy)
-#pragma unroll
-        for (int dx = 0; dx <= 2 * PR; ++dx) a = fmaf(p.w2[dy * (2 * PR + 1) + dx], m[dy * MW + dx] - c, a);
-      r = c + a;
-    } else if constexpr (POST == kPostBilateral) {
-      float acc = 0.0f, den = 0.0f;
+      float2 a = make_float2(0.f, 0.f);
 #pragma unroll
       for (int dy = 0; dy <= 2 * PR; ++dy)
 #pragma unroll
         for (int dx = 0; dx <= 2 * PR; ++dx) {
-          const float d = m[dy * MW + dx] - c;
-          const float w = exp2f(fmaf(p.kv * d, d, p.ks[dy * (2 * PR + 1) + dx]));
-          acc = fmaf(w, d, acc);
-          den += w;
+          const float2 d = __fadd2_rn(make_float2(m[dy * MW + dx], m[dy * MW + dx + 1]), make_float2(-c.x, -c.y));
+          const float w = p.w2[dy * (2 * PR + 1) + dx];
+          a = __ffma2_rn(make_float2(w, w), d, a);
         }
-      r = c + acc / den;
+      r = __fadd2_rn(c, a);
+    } else if constexpr (POST == kPostBilateral) {
+      float2 acc = make_float2(0.f, 0.f), den = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int dy = 0; dy <= 2 * PR; ++dy)
+#pragma unroll
+        for (int dx = 0; dx <= 2 * PR; ++dx) {
+          const float2 d = __fadd2_rn(make_float2(m[dy * MW + dx], m[dy * MW + dx + 1]), make_float2(-c.x, -c.y));
+          const float ks = p.ks[dy * (2 * PR + 1) + dx];
+          const float2 e = __ffma2_rn(__fmul2_rn(make_float2(p.kv, p.kv), d), d, make_float2(ks, ks));
+          const float2 w = make_float2(ex2_ftz(e.x), ex2_ftz(e.y));  // exponents <= 0
+          acc = __ffma2_rn(w, d, acc);
+          den = __fadd2_rn(den, w);
+        }
+      r = make_float2(c.x + __fdividef(acc.x, den.x), c.y + __fdividef(acc.y, den.y));
     }
-    if (PARTIAL && POST != kPostNone && !(c > kValid)) r = 0.0f;
-    __stcs(dst + (int64_t)gy * W + gx, r > kValid ? p.md - r : 0.0f);
+    float o[2] = {r.x, r.y};
+    const float cc[2] = {c.x, c.y};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (PARTIAL && POST != kPostNone && !(cc[h] > kValid)) o[h] = 0.0f;
+      o[h] = o[h] > kValid ? p.md - o[h] : 0.0f;
+    }
+    float* q = dst + (int64_t)gy * W + gx;
+    if (gx + 1 < W) {
+      if ((reinterpret_cast<uintptr_t>(q) & 7) == 0)
+        __stcs(reinterpret_cast<float2*>(q), make_float2(o[0], o[1]));
+      else
+        __stcs(q, o[0]), __stcs(q + 1, o[1]);
+    } else {
+      __stcs(q, o[0]);
+    }
   }
 }
 

@@ -5,11 +5,14 @@
 // (pipeline._blur_stage, pipeline.py:206-238; morphology.py:99-125;
 // depth_core.invert_back :150-156.)  Input: the stage-6 (FULL) or stage-4
 // (PARTIAL) map in the inverted encoding; output: the final direct-depth map.
-// One CTA per 64x32 output tile: the input tile (+ median and blur halos,
-// replicate-clamped) is staged in shared memory, the median is computed on
-// the tile plus the blur halo -- each halo position at its frame-clamped
-// centre, which is exactly the replicate border the reference's blur sees --
-// then the blur, re-impose and re-inversion run per output pixel.
+// One CTA per output tile (64 x 32 minus the blur halo): the input tile (+
+// median and blur halos, replicate-clamped) is staged in shared memory, the
+// median is computed on the tile plus the blur halo -- each halo position
+// outside the frame at its frame-clamped centre, which is exactly the
+// replicate border the reference's blur sees -- then the blur, re-impose and
+// re-inversion run two pixels per thread.  The 5x5 median uses one shared
+// min/max network per 4x2 block of outputs (median_block.cuh, ~70 min/max per
+// output instead of ~200 for a separate median-of-25 network).
 //
 // The median is exact (selection network, bit-identical to the reference's
 // median_network).  The Gaussian is fp32 centre-relative c + sum w_i w_j (q - c) and the
@@ -22,12 +25,16 @@
 #include <cmath>
 
 #include "dfc_common.cuh"
+#include "median_block.cuh"
 #include "median_networks.cuh"
 
 namespace dfc {
 namespace {
 
-constexpr int kTX = 64, kTY = 32, kThreads = 256;
+// The median region (output tile + blur halo) is kMW x kMH = 64 x 32: 256
+// blocks of 4 x 2 medians, one per thread.  Output tile = region - 2 PR.
+constexpr int kMW = 64, kMH = 32, kThreads = 256;
+static_assert((kMW / kMedBlockW) * (kMH / kMedBlockH) == kThreads, "one median block per thread");
 constexpr int kPostNone = 0, kPostGauss = 1, kPostBilateral = 2;
 
 struct TailParams {
@@ -72,8 +79,9 @@ template <int MR, int POST, int PR, bool PARTIAL>
 __global__ void __launch_bounds__(kThreads) blur_tail_kernel(const float* __restrict__ in, float* __restrict__ out,
                                                              int H, int W, const __grid_constant__ TailParams p) {
   constexpr int HI = MR + PR;                      // input halo
+  constexpr int kTX = kMW - 2 * PR, kTY = kMH - 2 * PR;
   constexpr int IW = kTX + 2 * HI, IH = kTY + 2 * HI;
-  constexpr int MW = kTX + 2 * PR, MH = kTY + 2 * PR;
+  constexpr int MW = kMW, MH = kMH;
   __shared__ float sIn[IH * IW];
   __shared__ float sM[MH * MW];
   const int64_t b = blockIdx.z;
@@ -88,6 +96,31 @@ __global__ void __launch_bounds__(kThreads) blur_tail_kernel(const float* __rest
   __syncthreads();
 
   // stage-7a: median (or copy) on the tile + blur halo, at frame-clamped centres
+  if constexpr (MR == 2) {
+    // shared 4x2-block network on the regular grid; positions outside the
+    // frame then take the value at their clamped position
+    const int bx = threadIdx.x % (MW / kMedBlockW), by = threadIdx.x / (MW / kMedBlockW);
+    const int mx = bx * kMedBlockW, my = by * kMedBlockH;
+    float med[kMedBlockH][kMedBlockW];
+    median5_block(sIn + my * IW + mx, IW, med);
+#pragma unroll
+    for (int j = 0; j < kMedBlockH; ++j)
+#pragma unroll
+      for (int c = 0; c < kMedBlockW; ++c) {
+        float v = med[j][c];
+        if (PARTIAL && !(sIn[(my + j + MR) * IW + mx + c + MR] > kValid)) v = 0.0f;
+        sM[(my + j) * MW + mx + c] = v;
+      }
+    if (x0 - PR < 0 || y0 - PR < 0 || x0 - PR + MW > W || y0 - PR + MH > H) {  // tile at a frame edge
+      __syncthreads();
+      for (int i = threadIdx.x; i < MH * MW; i += kThreads) {
+        const int py = i / MW, px = i - py * MW;
+        const int cy = clampi(y0 - PR + py, H) - y0 + PR, cx = clampi(x0 - PR + px, W) - x0 + PR;
+        const float v = sM[cy * MW + cx];  // an in-frame position: never rewritten here
+        if (cy != py || cx != px) sM[i] = v;
+      }
+    }
+  } else
   for (int i = threadIdx.x; i < MH * MW; i += kThreads) {
     const int my = i / MW, mx = i - my * MW;
     const int cy = clampi(y0 - PR + my, H) - y0 + HI;  // centre in sIn coordinates
@@ -160,6 +193,7 @@ __global__ void __launch_bounds__(kThreads) blur_tail_kernel(const float* __rest
 template <int MR, int POST, int PR>
 cudaError_t launch_t(const float* in, float* out, int64_t B, int H, int W, bool partial, const TailParams& p,
                      cudaStream_t s) {
+  constexpr int kTX = kMW - 2 * PR, kTY = kMH - 2 * PR;
   const dim3 grid((W + kTX - 1) / kTX, (H + kTY - 1) / kTY, (unsigned)B);
   note_launch();
   if (partial)

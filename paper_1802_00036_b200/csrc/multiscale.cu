@@ -145,16 +145,29 @@ __global__ void __launch_bounds__(kMsWarps * 32) ms_fast_kernel(const float* __r
       set_row(f2[i], 0.f);
   set_row(fd, 0.f);
   unsigned um = 0;
+  F4 nx[kB];  // next block's input rows, loaded one block ahead
+#pragma unroll
+  for (int j = 0; j < kB; ++j) {
+    if (j < H)
+      nx[j] = load4<VEC, true>(src + (int64_t)j * W, x0, W);
+    else
+      set_row(nx[j], 0.f);
+  }
   for (int t0 = 0; t0 < H + 3; t0 += kB) {
     const bool edge_rows = t0 < 3 || t0 + kB > H;
+    F4 cur[kB];
+#pragma unroll
+    for (int j = 0; j < kB; ++j) {
+      cur[j] = nx[j];
+      if (t0 + kB + j < H)
+        nx[j] = load4<VEC, true>(src + (int64_t)(t0 + kB + j) * W, x0, W);
+      else
+        set_row(nx[j], 0.f);
+    }
     F4 nv[kB], mv[kB], fv[kB];
 #pragma unroll
     for (int j = 0; j < kB; ++j) {
-      F4 d;
-      if (t0 + j < H)
-        d = load4<VEC, true>(src + (int64_t)(t0 + j) * W, x0, W);
-      else
-        set_row(d, 0.f);
+      const F4 d = cur[j];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const float v = d.v[c];

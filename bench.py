@@ -52,7 +52,7 @@ CONFIGS = {
         "fill_in_multiscale(max_depth=100, extrapolate=True, blur_type='bilateral', median_blur=True)"),
     3: ("gaussian", "full", False, 1024,
         "fill_in_fast(max_depth=100, 5x5 diamond, extrapolate=True, blur_type='gaussian')"),
-    4: ("median_bilateral", "full", True, 64,
+    4: ("median_bilateral", "full", True, 256,
         "fill_in_multiscale(max_depth=120, extrapolate=True, blur_type='bilateral', median_blur=True)"),
 }
 

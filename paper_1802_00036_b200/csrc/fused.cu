@@ -76,6 +76,7 @@ struct Params {
   const float* in;
   float* out;
   int64_t nframes;
+  int dense;  // shared-memory scratch for the dense large fill is available
   int H, W, strips, SW, nw;
   float md;
   float gw[5];
@@ -317,6 +318,56 @@ __device__ __forceinline__ float lf_one(const float* __restrict__ ring, int ring
   return __uint_as_float(__reduce_max_sync(kFull, m));
 }
 
+// Dense large fill (many empty pixels in a warp's 2-row pair): one pass for
+// the vertical 31-row maxima of both rows c0, c0+1 over the warp's columns
+// L-11 .. L+140 into V[2][kVC] (rows [c0-14, c0+15] are shared), then each lane
+// takes the horizontal 31-max of its own empty pixels from V.
+constexpr int kVC = 152, kVOff = 11, kDenseMin = 12;
+
+template <int PLAG>
+__device__ __noinline__ void lf_vpair(const float* __restrict__ ring, int ringw, int p0, int p1, int H, int L,
+                                      int lane, int c0, bool consecutive, float* __restrict__ V) {
+#pragma unroll 1
+  for (int sc = lane; sc < kVC; sc += 32) {
+    const int col = L - kVOff + sc;
+    float o0 = 0.f, o1 = 0.f;
+    if (col >= p0 && col < p1) {
+      const float* rc = ring + (col - p0);
+      auto ld = [&](int r) {
+        const int rr = r < 0 ? 0 : (r >= H ? H - 1 : r);
+        return rc[((rr + PLAG) % kRing) * ringw];
+      };
+      if (consecutive) {
+        float core = ld(c0 - 14);
+#pragma unroll 10
+        for (int r = c0 - 13; r <= c0 + 15; ++r) core = fmx(core, ld(r));
+        o0 = fmx(core, ld(c0 - 15));
+        o1 = fmx(core, ld(c0 + 16));
+      } else {  // frame ends: each row centre clamped separately
+        const int ca = min(max(c0, 0), H - 1), cb = min(max(c0 + 1, 0), H - 1);
+        float m = ld(ca - kLF);
+        for (int r = ca - kLF + 1; r <= ca + kLF; ++r) m = fmx(m, ld(r));
+        o0 = m;
+        m = ld(cb - kLF);
+        for (int r = cb - kLF + 1; r <= cb + kLF; ++r) m = fmx(m, ld(r));
+        o1 = m;
+      }
+    }
+    V[sc] = o0;
+    V[kVC + sc] = o1;
+  }
+  __syncwarp();
+}
+
+// horizontal 31-max of scratch row j around column x = L + 4 lane + c
+__device__ __forceinline__ float lf_hpixel(const float* __restrict__ V, int j, int lane, int c) {
+  const float* vr = V + j * kVC + 4 * lane + c + kVOff - kLF;
+  float m = vr[0];
+#pragma unroll 10
+  for (int d = 1; d <= 2 * kLF; ++d) m = fmx(m, vr[d]);
+  return m;
+}
+
 // ---------------------------------------------------------------------------
 // per-item state and one 4-row iteration (EDGE: rows may leave the frame)
 // ---------------------------------------------------------------------------
@@ -346,7 +397,7 @@ struct State {
   int srcL, srcR, compR;  // replicate sources for out-of-frame columns
 };
 
-template <int VEC, bool FULL, int BLUR, bool PRE, bool EDGE>
+template <int VEC, bool FULL, int BLUR, bool PRE, bool DENSE, bool EDGE>
 __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
   using LG = Lags<PRE>;
   const int H = p.H, W = p.W;
@@ -553,7 +604,27 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
         for (int c = 0; c < 4; ++c) em |= (unsigned)!(fmaxf(v6[j].v[c], S.nb[c]) > kValid) << (4 * j + c);
       S.had_empty |= em != 0;
       unsigned lanes = __ballot_sync(kFull, em != 0);
-      do {
+      if (DENSE && __reduce_add_sync(kFull, __popc(em)) > kDenseMin) {
+        float* V = S.ring + kRing * S.ringw + p.nw * (kB * 128) + (threadIdx.x >> 5) * (2 * kVC);
+#pragma unroll
+        for (int j2 = 0; j2 < kB; j2 += 2) {
+          if (!__any_sync(kFull, ((em >> (4 * j2)) & 0xFFu) != 0)) continue;
+          lf_vpair<LG::P>(S.ring, S.ringw, S.p0, S.p1, H, S.L, S.lane, tc0 + j2,
+                          !EDGE || (tc0 + j2 >= 0 && tc0 + j2 + 1 < H), V);
+#pragma unroll
+          for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              if (em >> (4 * (j2 + jj) + c) & 1u) {
+                const float r = lf_hpixel(V, jj, S.lane, c);
+                v6[j2 + jj].v[c] = r;
+                S.still_empty |= !(r > kValid);
+              }
+          __syncwarp();
+        }
+        lanes = 0;
+      }
+      while (lanes) {
         const int src = __ffs(lanes) - 1;
         lanes &= lanes - 1;
         unsigned pe = __shfl_sync(kFull, em, src);
@@ -571,7 +642,7 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
             S.still_empty |= !(r > kValid);
           }
         } while (pe);
-      } while (lanes);
+      }
     }
   }
   // out-of-frame columns replicate the edge column (the blur needs true replicate)
@@ -659,7 +730,7 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
 // ---------------------------------------------------------------------------
 // the fused kernel
 // ---------------------------------------------------------------------------
-template <int VEC, bool FULL, int BLUR, bool PRE>
+template <int VEC, bool FULL, int BLUR, bool PRE, bool DENSE>
 __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constant__ Params p) {
   using LG = Lags<PRE>;
   extern __shared__ __align__(16) float smem[];
@@ -761,9 +832,9 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
     const int kLo = (LG::C + 2 + kB - 1) / kB;  // tc0 - 2 >= 0 and tp >= 0
     const int kHi = (H - 2 * kB) / kB;           // t0 + 7 <= H - 1 and tc0 + 3 <= H - 1
     int k = 0;
-    for (; k < min(kLo, K); ++k) iterate<VEC, FULL, BLUR, PRE, true>(p, S, k);
-    for (; k <= kHi; ++k) iterate<VEC, FULL, BLUR, PRE, false>(p, S, k);
-    for (; k < K; ++k) iterate<VEC, FULL, BLUR, PRE, true>(p, S, k);
+    for (; k < min(kLo, K); ++k) iterate<VEC, FULL, BLUR, PRE, DENSE, true>(p, S, k);
+    for (; k <= kHi; ++k) iterate<VEC, FULL, BLUR, PRE, DENSE, false>(p, S, k);
+    for (; k < K; ++k) iterate<VEC, FULL, BLUR, PRE, DENSE, true>(p, S, k);
 
     // ---------------- per-frame flags ----------------
     const unsigned um = __reduce_max_sync(kFull, S.umax);
@@ -821,8 +892,11 @@ __global__ void finalize_kernel(const float* __restrict__ in, int64_t HW, const 
   }
 }
 
+constexpr size_t kSmemMax = 232448;  // 227 KB opt-in dynamic shared memory per CTA
+
 struct Layout {
   int strips, SW, nw, per_sm;  // per_sm: resident CTAs per SM (1)
+  bool dense;
   size_t smem;
 };
 
@@ -855,6 +929,10 @@ Layout layout_for(int W, int strips) {
   }
   const int ringw = (pwmax + 3) & ~3;
   L.smem = (size_t)kRing * ringw * 4 + (size_t)L.nw * kB * 512;
+  // dense large-fill scratch when it fits next to the ring (wide strips; a
+  // whole 1216-wide frame's ring leaves no room -- its empties are sparse)
+  L.dense = L.smem + (size_t)L.nw * 2 * kVC * 4 <= kSmemMax;
+  if (L.dense) L.smem += (size_t)L.nw * 2 * kVC * 4;
   L.per_sm = 1;
   return L;
 }
@@ -864,9 +942,9 @@ Layout layout_for(int W, int strips) {
 // strip halos and phase 1 are paid twice).
 Layout layout(int W) { return layout_for(W, W <= kStripMax ? 1 : (W + 1023) / 1024); }
 
-template <int VEC, bool FULL, int BLUR, bool PRE>
+template <int VEC, bool FULL, int BLUR, bool PRE, bool DENSE = false>
 cudaError_t launch_t(const Params& p, size_t smem, int grid, cudaStream_t s) {
-  auto k = fused_kernel<VEC, FULL, BLUR, PRE>;
+  auto k = fused_kernel<VEC, FULL, BLUR, PRE, DENSE>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   note_launch();
@@ -886,7 +964,18 @@ cudaError_t dispatch_blur(int blur, bool pre, const Params& p, size_t smem, int 
   return launch_t<VEC, FULL, kBlurRaw, false>(p, smem, grid, s);
 }
 
+// DENSE (shared-memory scratch for the dense large fill): FULL mode, wide strips, W % 4 == 0
+template <int BLUR>
+cudaError_t dispatch_dense(bool pre, const Params& p, size_t smem, int grid, cudaStream_t s) {
+  return pre ? launch_t<4, true, BLUR, true, true>(p, smem, grid, s) : launch_t<4, true, BLUR, false, true>(p, smem, grid, s);
+}
+
 cudaError_t dispatch(int vec, bool full, int blur, bool pre, const Params& p, size_t smem, int grid, cudaStream_t s) {
+  if (p.dense && vec == 4 && full) {
+    if (blur == DFC_BLUR_GAUSSIAN) return dispatch_dense<DFC_BLUR_GAUSSIAN>(pre, p, smem, grid, s);
+    if (blur == DFC_BLUR_NONE) return dispatch_dense<DFC_BLUR_NONE>(pre, p, smem, grid, s);
+    return dispatch_dense<kBlurRaw>(pre, p, smem, grid, s);
+  }
   if (vec == 4) return full ? dispatch_blur<4, true>(blur, pre, p, smem, grid, s)
                             : dispatch_blur<4, false>(blur, pre, p, smem, grid, s);
   if (vec == 2) return full ? dispatch_blur<2, true>(blur, pre, p, smem, grid, s)
@@ -908,7 +997,7 @@ bool fused_supported(const dfc_config& c, int H, int W) {
   if (!direct && !blur_tail_supported(c)) return false;
   if (H < 16 || W < 16) return false;
   const Layout L = layout(W);
-  return L.nw <= kNW && L.smem <= 232448;
+  return L.nw <= kNW && L.smem <= kSmemMax;
 }
 
 bool raw_mode(const dfc_config& c) {
@@ -946,6 +1035,7 @@ cudaError_t launch_fused(const float* in, float* out, int64_t B, int H, int W, c
   p.strips = L.strips;
   p.SW = L.SW;
   p.nw = L.nw;
+  p.dense = L.dense;
   p.md = c.max_depth;
   {
     const int r = c.gaussian_size / 2;

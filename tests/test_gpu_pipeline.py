@@ -364,3 +364,18 @@ def test_multiscale_other_kernels_vs_oracle(P, kernels):
     for i in range(frames.shape[0]):
         ref = O.complete(frames[i], O.OracleConfig(**{**_ocfg(kw).__dict__, "multiscale": ((15.0, 30.0), *kernels)}))
         _cmp(got[i], ref, "none")
+
+
+@pytest.mark.parametrize("blur", ["none", "gaussian", "median_bilateral"])
+def test_wide_sparse_frames_dense_large_fill(P, blur):
+    """~1% density on multi-strip frames: many empty pixels per warp block take
+    the dense large-fill path (shared vertical maxima) instead of per-pixel passes."""
+    spec = synth.SynthSpec(width=2600, height=256, beams=48, density=(0.008, 0.012))
+    frames = np.stack([synth.make_frame(spec, [950, i]) for i in range(2)])
+    kw = {"blur_mode": blur, "fill_mode": "full"}
+    res = P.complete_batch(frames, _pcfg(P, kw))
+    got = res.dense.cpu().numpy()
+    for i in range(frames.shape[0]):
+        ref, info = O.complete_with_stats(frames[i], _ocfg(kw))
+        _cmp(got[i], ref, blur)
+        assert int(res.iterations[i]) == info["large_fill_iterations"]

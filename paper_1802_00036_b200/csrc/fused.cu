@@ -1,856 +1,18 @@
-// Fused streaming depth-completion kernel for sm_100a (the hot path).
-//
-// One persistent CTA works on one (frame, column strip) item at a time; a
-// strip is the whole frame for W <= 1248.  Warps own ~104-column slices with
-// 12-column lane halos (32 lanes x 4 columns = 128 columns per warp), so all
-// horizontal neighbour traffic is warp shuffles and warps meet only at one
-// CTA barrier per 4-row block.  Columns outside the frame (one lane at the
-// left frame edge, >= 1 lane at the right edge) carry neutral values through
-// the min/max stages and replicated values into the blur, which reproduces
-// the reference's replicate border exactly.
-//
-// Phase 1 (FULL mode: extend_to_top needs each column's first valid row r0):
-//   top-down over 32-row blocks, validity bit-packed in 64-bit column words.
-//   The stage-4 validity equals the binary morphology D7(E5(D5(D_shape(M0))))
-//   of the input mask (SURVEY.md App. B probe 13), so r0 needs bit ops only.
-//   The scan stops once every owned column has its r0.
-// Phase 2: bottom-up streaming in 4-row blocks (going up, a column's r0 row
-//   comes before the rows above it, so extend_to_top needs no look-ahead).
-//   Producer (registers + shuffles): invert -> cross3 -> cross3 (= 5x5
-//   diamond) -> max5 -> min5 (close) -> masked max7 (small fill) -> extend.
-//   Stage-5 rows go to a 40-row shared-memory ring; the consumer runs 16 rows
-//   behind: 31x31 masked large fill (one warp-wide pass per empty pixel:
-//   lanes take the 31 window columns, redux.max combines them; typical
-//   frames hold ~50-200 such pixels), 5x5 Gaussian (fp32), invert back,
-//   coalesced store.
-//   Once the stage-5 rows are above every owned column's r0, stages 1-4 and
-//   the input reads stop: those rows are the captured top values.
-// Frames that still hold empties after one large-fill iteration are flagged
-// for the staged path (capi.cu: dfc_fill_finish).
-//
-// Reference semantics: depth_core.py:150-156 (invert), morphology.py:39-96
-// (dilate / close / masked fill / extend), pipeline.py:154-214 (stage order,
-// fill loop, blur, partial re-impose).  Every selection stage is bit-exact by
-// construction (min/max over clipped windows == replicate border); the
-// Gaussian is fp32 (<= 1e-4 m against the fp64 reference; tested).
-#include <cuda_runtime.h>
-#include <stdint.h>
-
-#include <climits>
-#include <cmath>
-#include <vector>
-
-#include "dfc_common.cuh"
-#include "lane_ops.cuh"
+// Fused streaming depth-completion kernel (csrc/fused_impl.cuh): host side --
+// layout, workspace, chunked rounds (multiscale stage 2 -> fused -> blur tail)
+// and the per-frame status finalize kernel.
+#include "fused_impl.cuh"
 
 namespace dfc {
+
+cudaError_t fused_dispatch_vec4(bool full, int blur, bool pre, bool dense, const void* params, size_t smem, int grid,
+                                cudaStream_t s);
+cudaError_t fused_dispatch_vec2(bool full, int blur, bool pre, bool dense, const void* params, size_t smem, int grid,
+                                cudaStream_t s);
+cudaError_t fused_dispatch_vec1(bool full, int blur, bool pre, bool dense, const void* params, size_t smem, int grid,
+                                cudaStream_t s);
+
 namespace {
-
-constexpr int kNW = 12;                // warps per CTA
-constexpr int kLW = 128;               // columns per warp (32 lanes x 4)
-constexpr int kHalo = 12;              // lane-halo columns per side (9 morphology + 2 blur, lane aligned)
-constexpr int kRing = 40;              // stage-5 ring rows (39 live)
-constexpr int kRingBlocks = kRing / kB;
-constexpr int kLag = 16;               // consumer lag behind the stage-5 producer (>= 15)
-// Row lags (processing order).  Stage 5 trails the input by 1+1+2+2+3 = 9
-// rows (cross3, cross3, max5, min5, max7); with a precomputed stage-2 map
-// (PRE: multiscale) by 2+2+3 = 7.  The consumer trails stage 5 by kLag; its
-// first block is the one whose rows start in [-3, 0].
-template <bool PRE>
-struct Lags {
-  static constexpr int L2 = PRE ? 0 : 2;  // stage-2 lag
-  static constexpr int P = L2 + 7;        // stage-5 lag
-  static constexpr int C = P + kLag;      // consumer rows = t0 - C + j
-  static constexpr int KFirst = C / kB;
-};
-constexpr int kLF = 15;                // large fill radius
-constexpr int kStripMax = 1248;        // widest strip handled by one CTA
-constexpr uint32_t kNeedsStaged = 0x200u;  // internal status bit (capi.cu)
-constexpr int kBlurRaw = -1;           // emit the stage-6 (FULL) / stage-4 (PARTIAL) inverted map for blur_tail.cu
-constexpr int64_t kRawChunk = 296;     // frames per fused -> blur-tail round (2 per SM) in the raw mode
-
-static_assert(kRing % kB == 0 && kLag % kB == 0, "ring blocks must not wrap inside a block");
-
-
-struct Params {
-  const float* in;
-  float* out;
-  int64_t nframes;
-  int dense;  // shared-memory scratch for the dense large fill is available
-  int H, W, strips, SW, nw;
-  float md;
-  float gw[5];
-  float2 gh[6];  // horizontal pass on column pairs: coefficients of e[i] for outputs (c, c+1)
-  uint32_t* status;
-  int32_t* iters;
-  unsigned long long* nfallback;
-  unsigned* work;
-  unsigned* umax;
-};
-
-// Stage one lane's 4 columns of an input row into shared memory with cp.async
-// (zero-filled where the row or the columns lie outside the frame).
-template <int BYTES>
-__device__ __forceinline__ void cp_async_zfill(uint32_t sdst, const void* gsrc, bool ok) {
-  const int n = ok ? BYTES : 0;
-  if constexpr (BYTES == 16)
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sdst), "l"(gsrc), "r"(n) : "memory");
-  else
-    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(sdst), "l"(gsrc), "n"(BYTES), "r"(n)
-                 : "memory");
-}
-
-template <int VEC>
-__device__ __forceinline__ void stage_lane(uint32_t sdst, const float* q, const float* safe, bool rowok, bool full,
-                                           unsigned incol) {
-  if constexpr (VEC == 4) {
-    const bool ok = rowok && full;
-    cp_async_zfill<16>(sdst, ok ? q : safe, ok);
-  } else if constexpr (VEC == 2) {
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const bool ok = rowok && ((incol >> (2 * h)) & 3u) == 3u;
-      cp_async_zfill<8>(sdst + 8 * h, ok ? q + 2 * h : safe, ok);
-    }
-  } else {
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const bool ok = rowok && (incol >> c & 1);
-      cp_async_zfill<4>(sdst + 4 * c, ok ? q + c : safe, ok);
-    }
-  }
-}
-
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
-
-__device__ __forceinline__ F4 lds4(uint32_t saddr) {
-  float4 q;
-  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n" : "=f"(q.x), "=f"(q.y), "=f"(q.z), "=f"(q.w) : "r"(saddr)
-               : "memory");
-  return F4{{q.x, q.y, q.z, q.w}};
-}
-
-// ---------------------------------------------------------------------------
-// per-item warp geometry
-// ---------------------------------------------------------------------------
-struct Geo {
-  int o0, o1;  // output columns of the strip
-  int p0, p1;  // stage-5 production (ring) columns
-  int L;       // first lane column of this warp (-4 at the left frame edge)
-  int q0, q1;  // stage-5 columns this warp owns (writes to the ring); empty for spare warps
-};
-
-__device__ __forceinline__ int warp_q1(int L, int q0, int p1, int W) {
-  if (p1 == W && L + kLW - 4 >= W) return W;  // right frame edge, >= 1 out-of-frame lane
-  return min(p1, L + kLW - kHalo);
-}
-
-__device__ void item_geometry(int s, const Params& p, int warp, Geo& g) {
-  g.o0 = s * p.SW;
-  g.o1 = min(p.W, g.o0 + p.SW);
-  g.p0 = g.o0 == 0 ? 0 : max(0, (g.o0 - 17) & ~3);
-  g.p1 = g.o1 == p.W ? p.W : min(p.W, (g.o1 + 17 + 3) & ~3);
-  int q0 = g.p0, L = 0, q1 = 0;
-  for (int w = 0; w <= warp; ++w) {
-    if (q0 >= g.p1) {  // spare warp: duplicate the last one, own nothing
-      q0 = q1 = g.p1;
-      break;
-    }
-    L = q0 == 0 ? -4 : q0 - kHalo;
-    q1 = warp_q1(L, q0, g.p1, p.W);
-    if (w < warp) q0 = q1;
-  }
-  g.L = L;
-  g.q0 = q0;
-  g.q1 = q1;
-}
-
-// ---------------------------------------------------------------------------
-// Phase 1: first valid stage-4 row per column, bit-packed morphology
-// ---------------------------------------------------------------------------
-// bit i of w[c]: (inverted) validity of row y0 + i; PRE: the frame is the
-// stage-2 map in the inverted encoding already
-template <int VEC, bool PRE>
-__device__ __forceinline__ void load_bits(const float* frame, int H, int W, int x0, int y0, float md, uint32_t w[4],
-                                          unsigned& umax) {
-#pragma unroll
-  for (int c = 0; c < 4; ++c) w[c] = 0;
-  if (y0 >= H) return;
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    F4 v[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int y = y0 + 16 * h + i;
-      if (y < H)
-        v[i] = load4<VEC, false>(frame + (int64_t)y * W, x0, W);
-      else
-        set_row(v[i], 0.f);
-    }
-#pragma unroll
-    for (int i = 0; i < 16; ++i)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        if constexpr (PRE) {
-          w[c] |= (uint32_t)(v[i].v[c] > kValid) << (16 * h + i);
-        } else {
-          umax = max(umax, __float_as_uint(v[i].v[c]));
-          const float inv = v[i].v[c] > kValid ? md - v[i].v[c] : 0.0f;
-          w[c] |= (uint32_t)(inv > kValid) << (16 * h + i);
-        }
-      }
-  }
-}
-
-__device__ __forceinline__ uint64_t vdil(uint64_t x, int r) {
-  uint64_t o = x;
-  for (int i = 1; i <= r; ++i) o |= (x << i) | (x >> i);
-  return o;
-}
-
-__device__ __forceinline__ uint64_t vero(uint64_t x, int r) {
-  uint64_t o = x;
-  for (int i = 1; i <= r; ++i) o &= (x << i) & (x >> i);
-  return o;
-}
-
-template <int R, bool AND>
-__device__ __forceinline__ void hcomb(const uint64_t in[4], uint64_t out[4]) {
-  uint64_t e[4 + 2 * R];
-#pragma unroll
-  for (int i = 0; i < R; ++i) {
-    e[R - 1 - i] = __shfl_up_sync(kFull, in[3 - i], 1);
-    e[R + 4 + i] = __shfl_down_sync(kFull, in[i], 1);
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) e[R + i] = in[i];
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    uint64_t a = e[c];
-#pragma unroll
-    for (int d = 1; d <= 2 * R; ++d) a = AND ? (a & e[c + d]) : (a | e[c + d]);
-    out[c] = a;
-  }
-}
-
-template <int VEC, bool PRE>
-__device__ __forceinline__ void phase1(const float* frame, const Params& p, int x0, bool needed, unsigned incol,
-                                       int T0[4], unsigned& umax) {
-  const int H = p.H, W = p.W;
-  uint32_t prv[4] = {0, 0, 0, 0}, cur[4], nxt[4];
-  load_bits<VEC, PRE>(frame, H, W, x0, 0, p.md, cur, umax);
-  load_bits<VEC, PRE>(frame, H, W, x0, 32, p.md, nxt, umax);
-  int r0[4] = {-1, -1, -1, -1};
-  uint64_t cm[4];
-#pragma unroll
-  for (int c = 0; c < 4; ++c) cm[c] = (incol >> c & 1) ? ~0ull : 0ull;
-  for (int b = 0; 32 * b < H; ++b) {
-    uint64_t X[4], A[4], Bq[4];
-    const int lo = max(0, 16 - 32 * b), hi = min(64, H - 32 * b + 16);
-    const uint64_t inrow = (hi <= lo) ? 0ull : ((hi - lo == 64) ? ~0ull : (((1ull << (hi - lo)) - 1) << lo));
-#pragma unroll
-    for (int c = 0; c < 4; ++c)
-      X[c] = ((uint64_t)(prv[c] >> 16) | ((uint64_t)cur[c] << 16) | ((uint64_t)nxt[c] << 48)) & cm[c];
-    // D_shape = cross3 o cross3 (5x5 diamond); PRE: the stage-2 validity is loaded
-#pragma unroll
-    for (int it = 0; it < (PRE ? 0 : 2); ++it) {
-      hcomb<1, false>(X, A);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) Bq[c] = (vdil(X[c], 1) | A[c]) & inrow & cm[c];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) X[c] = Bq[c];
-    }
-    // D5
-#pragma unroll
-    for (int c = 0; c < 4; ++c) A[c] = vdil(X[c], 2);
-    hcomb<2, false>(A, Bq);
-    // E5: outside the frame counts as set (clipped window)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) A[c] = vero((Bq[c] & inrow & cm[c]) | ~(inrow & cm[c]), 2);
-    hcomb<2, true>(A, Bq);
-    // D7
-#pragma unroll
-    for (int c = 0; c < 4; ++c) A[c] = vdil(Bq[c] & inrow & cm[c], 3);
-    hcomb<3, false>(A, Bq);
-    bool done = true;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const uint32_t cand = (uint32_t)((Bq[c] & inrow & cm[c]) >> 16);
-      if (r0[c] < 0 && cand) r0[c] = 32 * b + __ffs(cand) - 1;
-      done = done && (r0[c] >= 0 || !(incol >> c & 1));
-    }
-    if (__all_sync(kFull, done || !needed)) break;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      prv[c] = cur[c];
-      cur[c] = nxt[c];
-    }
-    load_bits<VEC, PRE>(frame, H, W, x0, 32 * (b + 2), p.md, nxt, umax);
-  }
-#pragma unroll
-  for (int c = 0; c < 4; ++c) T0[c] = r0[c] >= 0 ? (H - 1 - r0[c]) : INT_MAX;
-}
-
-// ---------------------------------------------------------------------------
-// Large masked fill of one empty pixel (x, row), warp-cooperative: lane i
-// takes column x - 15 + i (i < 31) and the max over ring rows [row-15,
-// row+15] (clamped == clipped for max); columns outside [p0, p1) lie outside
-// the frame (the strip's ring covers every needed window) and count as 0.
-// Stage-5 values are >= 0, so their float bit patterns order like the values
-// and one redux.max combines the lanes.
-// ---------------------------------------------------------------------------
-template <int PLAG>
-__device__ __forceinline__ float lf_one(const float* __restrict__ ring, int ringw, int p0, int p1, int H, int lane,
-                                        int x, int row) {
-  const int col = x - kLF + lane;
-  unsigned m = 0u;
-  if (lane < 2 * kLF + 1 && col >= p0 && col < p1) {
-    const float* rc = ring + (col - p0);
-    const int r0 = max(row - kLF, 0), r1 = min(row + kLF, H - 1);
-    int slot = (r0 + PLAG) % kRing;
-#pragma unroll 8
-    for (int r = r0; r <= r1; ++r) {
-      m = max(m, __float_as_uint(rc[slot * ringw]));
-      slot = slot + 1 == kRing ? 0 : slot + 1;
-    }
-  }
-  return __uint_as_float(__reduce_max_sync(kFull, m));
-}
-
-// Dense large fill (many empty pixels in a warp's 2-row pair): one pass for
-// the vertical 31-row maxima of both rows c0, c0+1 over the warp's columns
-// L-11 .. L+140 into V[2][kVC] (rows [c0-14, c0+15] are shared), then each lane
-// takes the horizontal 31-max of its own empty pixels from V.
-constexpr int kVC = 152, kVOff = 11, kDenseMin = 12;
-
-template <int PLAG>
-__device__ __noinline__ void lf_vpair(const float* __restrict__ ring, int ringw, int p0, int p1, int H, int L,
-                                      int lane, int c0, bool consecutive, float* __restrict__ V) {
-#pragma unroll 1
-  for (int sc = lane; sc < kVC; sc += 32) {
-    const int col = L - kVOff + sc;
-    float o0 = 0.f, o1 = 0.f;
-    if (col >= p0 && col < p1) {
-      const float* rc = ring + (col - p0);
-      auto ld = [&](int r) {
-        const int rr = r < 0 ? 0 : (r >= H ? H - 1 : r);
-        return rc[((rr + PLAG) % kRing) * ringw];
-      };
-      if (consecutive) {
-        float core = ld(c0 - 14);
-#pragma unroll 10
-        for (int r = c0 - 13; r <= c0 + 15; ++r) core = fmx(core, ld(r));
-        o0 = fmx(core, ld(c0 - 15));
-        o1 = fmx(core, ld(c0 + 16));
-      } else {  // frame ends: each row centre clamped separately
-        const int ca = min(max(c0, 0), H - 1), cb = min(max(c0 + 1, 0), H - 1);
-        float m = ld(ca - kLF);
-        for (int r = ca - kLF + 1; r <= ca + kLF; ++r) m = fmx(m, ld(r));
-        o0 = m;
-        m = ld(cb - kLF);
-        for (int r = cb - kLF + 1; r <= cb + kLF; ++r) m = fmx(m, ld(r));
-        o1 = m;
-      }
-    }
-    V[sc] = o0;
-    V[kVC + sc] = o1;
-  }
-  __syncwarp();
-}
-
-// horizontal 31-max of scratch row j around column x = L + 4 lane + c
-__device__ __forceinline__ float lf_hpixel(const float* __restrict__ V, int j, int lane, int c) {
-  const float* vr = V + j * kVC + 4 * lane + c + kVOff - kLF;
-  float m = vr[0];
-#pragma unroll 10
-  for (int d = 1; d <= 2 * kLF; ++d) m = fmx(m, vr[d]);
-  return m;
-}
-
-// ---------------------------------------------------------------------------
-// per-item state and one 4-row iteration (EDGE: rows may leave the frame)
-// ---------------------------------------------------------------------------
-struct State {
-  const float* rring;  // consumer read base: ring + clamped lane column
-  float* wring;        // producer write base: ring + lane column (owned lanes only)
-  float* ring;
-  int ringw, x0, lane, L, p0, p1;
-  unsigned own, outm, oob, oobL, oobR;
-  bool woob;
-  float nb[4];  // -FMAX where the consumer needs the column, +FMAX elsewhere
-  int T0[4];
-  float top[4];
-  int tmin, tmax;
-  int tmaxN;           // max r0 row (processing order) over the columns the consumer needs
-  bool skip, fast;
-  F4 c1[2], c2[2], c3[4], c4[4], c5[6], gc[4], mprev[2];
-  F4 ofast;            // output row above every needed r0 (FULL): all such rows are equal
-  uint32_t stg;        // shared-memory staging slot of this lane (row j at +512 j)
-  const float* lrow;   // input row of processing row t0 + kB at column x0
-  float* orow;         // output row of processing row tc0 - 2 at column x0
-  bool full;           // all 4 columns inside the frame
-  unsigned incol;
-  float amin;          // FULL: min blurred value (<= 0.1 sends the frame to the staged path)
-  unsigned umax;
-  bool had_empty, still_empty;
-  int srcL, srcR, compR;  // replicate sources for out-of-frame columns
-};
-
-template <int VEC, bool FULL, int BLUR, bool PRE, bool DENSE, bool EDGE>
-__device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
-  using LG = Lags<PRE>;
-  const int H = p.H, W = p.W;
-  const int t0 = kB * k;
-  const int tp = t0 - LG::P;
-  constexpr int L2 = LG::L2;
-  // ======================= producer =======================
-  if (FULL && !S.skip && tp > S.tmax) S.skip = true;
-  F4 f[kB];
-  if (!S.skip) {
-    F4 a[kB];
-    cp_async_wait_all();  // this block's rows, staged one block ago
-#pragma unroll
-    for (int j = 0; j < kB; ++j) {
-      a[j] = lds4(S.stg + j * 512);
-      if constexpr (!PRE) {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const float v = a[j].v[c];
-          S.umax = max(S.umax, __float_as_uint(v));
-          a[j].v[c] = v > kValid ? p.md - v : 0.0f;
-        }
-      }
-    }
-    // stage the next block; stops once its stage-5 rows lie above every r0.
-    // The values read above are materialised first: the shared reads are
-    // complete before the slot is overwritten.
-    if constexpr (PRE) {
-#pragma unroll
-      for (int j = 0; j < kB; ++j)
-        asm volatile("" ::"f"(a[j].v[0]), "f"(a[j].v[1]), "f"(a[j].v[2]), "f"(a[j].v[3]));
-    } else {
-      asm volatile("" ::"r"(S.umax));
-    }
-    if (!FULL || (t0 + kB - LG::P <= S.tmax)) {
-      const float* q = S.lrow;
-#pragma unroll
-      for (int j = 0; j < kB; ++j, q -= W)
-        stage_lane<VEC>(S.stg + j * 512, q, p.in, !EDGE || t0 + kB + j < H, S.full, S.incol);
-      cp_async_commit();
-    }
-    // --- stage 2: cross3 o cross3 = 5x5 diamond (rows t0-2+j); PRE: the staged rows ---
-    F4 d2[kB];
-    if constexpr (PRE) {
-#pragma unroll
-      for (int j = 0; j < kB; ++j) d2[j] = a[j];  // rows >= H and out-of-frame columns were staged as 0
-    } else {
-    F4 d1[kB];
-    {
-      const F4 in[kB + 2] = {S.c1[0], S.c1[1], a[0], a[1], a[2], a[3]};
-#pragma unroll
-      for (int j = 0; j < kB; ++j) {
-        const Ext<1> e = ext_row<1>(in[j + 1]);
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-          d1[j].v[c] = fmx3(fmx3(in[j].v[c], in[j + 1].v[c], in[j + 2].v[c]), e.e[c], e.e[c + 2]);
-      }
-      S.c1[0] = a[2], S.c1[1] = a[3];
-#pragma unroll
-      for (int j = 0; j < kB; ++j) {
-        if (EDGE && (t0 - 1 + j < 0 || t0 - 1 + j >= H)) set_row(d1[j], 0.f);
-        if (S.woob) fix_oob(d1[j], S.oob, 0.f);
-      }
-    }
-    // --- cross3 #2 (rows t0-2+j) ---
-    {
-      const F4 in[kB + 2] = {S.c2[0], S.c2[1], d1[0], d1[1], d1[2], d1[3]};
-#pragma unroll
-      for (int j = 0; j < kB; ++j) {
-        const Ext<1> e = ext_row<1>(in[j + 1]);
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-          d2[j].v[c] = fmx3(fmx3(in[j].v[c], in[j + 1].v[c], in[j + 2].v[c]), e.e[c], e.e[c + 2]);
-      }
-      S.c2[0] = d1[2], S.c2[1] = d1[3];
-#pragma unroll
-      for (int j = 0; j < kB; ++j) {
-        if (EDGE && (t0 - 2 + j < 0 || t0 - 2 + j >= H)) set_row(d2[j], 0.f);
-        if (S.woob) fix_oob(d2[j], S.oob, 0.f);
-      }
-    }
-    }
-    // --- close: max5 (rows t0-L2-2+j) ---
-    F4 m5[kB];
-    {
-      const F4 in[kB + 4] = {S.c3[0], S.c3[1], S.c3[2], S.c3[3], d2[0], d2[1], d2[2], d2[3]};
-      F4 vv[kB];
-      vwin2<OpMax>(in, vv);
-#pragma unroll
-      for (int j = 0; j < kB; ++j) m5[j] = hwin2<OpMax>(ext_row<2>(vv[j]));
-#pragma unroll
-      for (int i = 0; i < 4; ++i) S.c3[i] = d2[i];
-#pragma unroll
-      for (int j = 0; j < kB; ++j) {
-        if (EDGE && (t0 - L2 - 2 + j < 0 || t0 - L2 - 2 + j >= H)) set_row(m5[j], kFMax);
-        if (S.woob) fix_oob(m5[j], S.oob, kFMax);
-      }
-    }
-    // --- close: min5 (rows t0-L2-4+j) ---
-    F4 cl[kB];
-    {
-      const F4 in[kB + 4] = {S.c4[0], S.c4[1], S.c4[2], S.c4[3], m5[0], m5[1], m5[2], m5[3]};
-      F4 vv[kB];
-      vwin2<OpMin>(in, vv);
-#pragma unroll
-      for (int j = 0; j < kB; ++j) cl[j] = hwin2<OpMin>(ext_row<2>(vv[j]));
-#pragma unroll
-      for (int i = 0; i < 4; ++i) S.c4[i] = m5[i];
-#pragma unroll
-      for (int j = 0; j < kB; ++j) {
-        if (EDGE && (t0 - L2 - 4 + j < 0 || t0 - L2 - 4 + j >= H)) set_row(cl[j], 0.f);
-        if (S.woob) fix_oob(cl[j], S.oob, 0.f);
-      }
-    }
-    // --- small fill: masked max7 (rows t0-L2-7+j = tp+j) ---
-    {
-      const F4 in[kB + 6] = {S.c5[0], S.c5[1], S.c5[2], S.c5[3], S.c5[4], S.c5[5], cl[0], cl[1], cl[2], cl[3]};
-      F4 vv[kB];
-      vwin3<OpMax>(in, vv);
-#pragma unroll
-      for (int j = 0; j < kB; ++j) {
-        const F4 h7 = hwin3<OpMax>(ext_row<3>(vv[j]));
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const float ctr = in[j + 3].v[c];
-          f[j].v[c] = ctr > kValid ? ctr : h7.v[c];
-        }
-      }
-      S.c5[0] = S.c5[4], S.c5[1] = S.c5[5];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) S.c5[i + 2] = cl[i];
-    }
-    // --- extend to top (FULL; only blocks reaching some column's r0) ---
-    if (FULL && tp + kB - 1 >= S.tmin) {
-#pragma unroll
-      for (int j = 0; j < kB; ++j) {
-        const int t = tp + j;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          if (t == S.T0[c]) S.top[c] = f[j].v[c];
-          if (t > S.T0[c]) f[j].v[c] = S.top[c];
-        }
-      }
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < kB; ++j)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) f[j].v[c] = S.top[c];
-  }
-  S.lrow -= kB * W;
-  // --- ring store: ring slot of row t is (t + P) mod 40, so this block is slots 4*(k mod 10) + j ---
-  if (S.own) {
-    float* w = S.wring + (k % kRingBlocks) * kB * S.ringw;
-#pragma unroll
-    for (int j = 0; j < kB; ++j)
-      if (!EDGE || (tp + j >= 0 && tp + j < H))
-        *reinterpret_cast<float4*>(w + j * S.ringw) = make_float4(f[j].v[0], f[j].v[1], f[j].v[2], f[j].v[3]);
-  }
-  __syncthreads();
-  // ======================= consumer =======================
-  const int tc0 = t0 - LG::C;
-  if (k < LG::KFirst) return;
-  float* orow = S.orow;  // output row of processing row tc0 - 2
-  S.orow -= kB * W;
-  if (FULL && S.fast) {
-    // every row of the blur windows lies above each needed column's r0: the
-    // stage-6 rows are the captured top values and every output row is equal
-#pragma unroll
-    for (int j = 0; j < kB; ++j, orow -= W) {
-      const int t = tc0 - 2 + j;
-      if (EDGE && (t < 0 || t >= H)) continue;
-      if (S.outm) store_lane<VEC>(orow, S.ofast, S.outm);
-    }
-    return;
-  }
-  F4 v6[kB];
-  {
-    // rows tc0 + j live in slots 4*((k + 6) mod 10) + j when inside the frame
-    const float* r = S.rring + ((k + kRingBlocks - kLag / kB) % kRingBlocks) * kB * S.ringw;
-#pragma unroll
-    for (int j = 0; j < kB; ++j) {
-      const float* rr = r + j * S.ringw;
-      if (EDGE) {
-        const int t = min(max(tc0 + j, 0), H - 1);
-        rr = S.rring + ((t + LG::P) % kRing) * S.ringw;
-      }
-      const float4 q = *reinterpret_cast<const float4*>(rr);
-      v6[j].v[0] = q.x, v6[j].v[1] = q.y, v6[j].v[2] = q.z, v6[j].v[3] = q.w;
-    }
-  }
-  if (FULL) {
-    // any needed empty pixel in this block? (max with nb masks unneeded columns)
-    float mn = kFMax;
-#pragma unroll
-    for (int j = 0; j < kB; ++j)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) mn = fminf(mn, fmaxf(v6[j].v[c], S.nb[c]));
-    if (__any_sync(kFull, !(mn > kValid))) {
-      unsigned em = 0;  // bit 4j+c: needed empty pixel
-#pragma unroll
-      for (int j = 0; j < kB; ++j)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) em |= (unsigned)!(fmaxf(v6[j].v[c], S.nb[c]) > kValid) << (4 * j + c);
-      S.had_empty |= em != 0;
-      unsigned lanes = __ballot_sync(kFull, em != 0);
-      if (DENSE && __reduce_add_sync(kFull, __popc(em)) > kDenseMin) {
-        float* V = S.ring + kRing * S.ringw + p.nw * (kB * 128) + (threadIdx.x >> 5) * (2 * kVC);
-#pragma unroll
-        for (int j2 = 0; j2 < kB; j2 += 2) {
-          if (!__any_sync(kFull, ((em >> (4 * j2)) & 0xFFu) != 0)) continue;
-          lf_vpair<LG::P>(S.ring, S.ringw, S.p0, S.p1, H, S.L, S.lane, tc0 + j2,
-                          !EDGE || (tc0 + j2 >= 0 && tc0 + j2 + 1 < H), V);
-#pragma unroll
-          for (int jj = 0; jj < 2; ++jj)
-#pragma unroll
-            for (int c = 0; c < 4; ++c)
-              if (em >> (4 * (j2 + jj) + c) & 1u) {
-                const float r = lf_hpixel(V, jj, S.lane, c);
-                v6[j2 + jj].v[c] = r;
-                S.still_empty |= !(r > kValid);
-              }
-          __syncwarp();
-        }
-        lanes = 0;
-      }
-      while (lanes) {
-        const int src = __ffs(lanes) - 1;
-        lanes &= lanes - 1;
-        unsigned pe = __shfl_sync(kFull, em, src);
-        do {
-          const int b = __ffs(pe) - 1;
-          pe &= pe - 1;
-          const int row = EDGE ? min(max(tc0 + (b >> 2), 0), H - 1) : tc0 + (b >> 2);
-          const float r = lf_one<LG::P>(S.ring, S.ringw, S.p0, S.p1, H, S.lane, S.L + 4 * src + (b & 3), row);
-          if (S.lane == src) {
-#pragma unroll
-            for (int j = 0; j < kB; ++j)
-#pragma unroll
-              for (int c = 0; c < 4; ++c)
-                if (b == 4 * j + c) v6[j].v[c] = r;
-            S.still_empty |= !(r > kValid);
-          }
-        } while (pe);
-      }
-    }
-  }
-  // out-of-frame columns replicate the edge column (the blur needs true replicate)
-  if (S.woob) {
-#pragma unroll
-    for (int j = 0; j < kB; ++j) {
-      const float eL = __shfl_sync(kFull, v6[j].v[0], S.srcL);
-      const float sr = S.compR == 0 ? v6[j].v[0] : (S.compR == 1 ? v6[j].v[1] : (S.compR == 2 ? v6[j].v[2] : v6[j].v[3]));
-      const float eR = __shfl_sync(kFull, sr, S.srcR);
-      fix_oob(v6[j], S.oobL, eL);
-      fix_oob(v6[j], S.oobR, eR);
-    }
-  }
-  if constexpr (BLUR == DFC_BLUR_GAUSSIAN) {
-    F4 h[kB];
-#pragma unroll
-    for (int j = 0; j < kB; ++j) {
-      const Ext<2> e = ext_row<2>(v6[j]);
-#pragma unroll
-      for (int hp = 0; hp < 2; ++hp) {  // packed fp32x2: outputs (2hp, 2hp+1), inputs broadcast
-        const float* x = e.e + 2 * hp;
-        float2 a = __fmul2_rn(make_float2(x[0], x[0]), p.gh[0]);
-#pragma unroll
-        for (int i = 1; i < 6; ++i) a = __ffma2_rn(make_float2(x[i], x[i]), p.gh[i], a);
-        h[j].v[2 * hp] = a.x;
-        h[j].v[2 * hp + 1] = a.y;
-      }
-    }
-    if (EDGE && k == LG::KFirst) {  // rows above row 0 replicate it (tc0 in [-3, 0]: h[0] is row 0)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) S.gc[i] = h[0];
-    }
-    const F4 in[kB + 4] = {S.gc[0], S.gc[1], S.gc[2], S.gc[3], h[0], h[1], h[2], h[3]};
-#pragma unroll
-    for (int i = 0; i < 4; ++i) S.gc[i] = h[i];
-    F4 mk[kB];
-    if (!FULL) {  // pre-blur validity of output rows tc0-2+j (pipeline.py:212-214)
-      mk[0] = S.mprev[0], mk[1] = S.mprev[1], mk[2] = v6[0], mk[3] = v6[1];
-      S.mprev[0] = v6[2], S.mprev[1] = v6[3];
-    }
-    F4 o;
-#pragma unroll
-    for (int j = 0; j < kB; ++j, orow -= W) {
-      const int t = tc0 + j - 2;  // output row (processing order)
-      if (EDGE && (t < 0 || t >= H)) continue;
-#pragma unroll
-      for (int hp = 0; hp < 2; ++hp) {  // packed fp32x2 over the column pair (2hp, 2hp+1)
-        const int c = 2 * hp;
-        float2 a = __fmul2_rn(make_float2(in[j].v[c], in[j].v[c + 1]), make_float2(p.gw[0], p.gw[0]));
-#pragma unroll
-        for (int i = 1; i < 5; ++i)
-          a = __ffma2_rn(make_float2(in[j + i].v[c], in[j + i].v[c + 1]), make_float2(p.gw[i], p.gw[i]), a);
-        const float2 r = __ffma2_rn(a, make_float2(-1.f, -1.f), make_float2(p.md, p.md));  // md - a, exact negation
-        o.v[c] = a.x > kValid ? r.x : 0.0f;
-        o.v[c + 1] = a.y > kValid ? r.y : 0.0f;
-        if (!FULL && !(mk[j].v[c] > kValid)) o.v[c] = 0.0f;
-        if (!FULL && !(mk[j].v[c + 1] > kValid)) o.v[c + 1] = 0.0f;
-      }
-      if (S.outm) store_lane<VEC>(orow, o, S.outm);
-    }
-    // rows tc0-4 .. tc0+3 above every needed r0: output row tc0+1 repeats from here on
-    if (FULL && !EDGE && tc0 - 4 > S.tmaxN) {
-      S.fast = true;
-      S.ofast = o;
-    }
-  } else {
-    orow -= 2 * W;  // no blur: output rows are tc0 + j
-    F4 o;
-#pragma unroll
-    for (int j = 0; j < kB; ++j, orow -= W) {
-      const int t = tc0 + j;
-      if (EDGE && (t < 0 || t >= H)) continue;
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        o.v[c] = BLUR == kBlurRaw ? v6[j].v[c] : (v6[j].v[c] > kValid ? p.md - v6[j].v[c] : 0.0f);
-      if (S.outm) store_lane<VEC>(orow, o, S.outm);
-    }
-    if (FULL && !EDGE && tc0 > S.tmaxN) {
-      S.fast = true;
-      S.ofast = o;
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// the fused kernel
-// ---------------------------------------------------------------------------
-template <int VEC, bool FULL, int BLUR, bool PRE, bool DENSE>
-__global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constant__ Params p) {
-  using LG = Lags<PRE>;
-  extern __shared__ __align__(16) float smem[];
-  __shared__ unsigned s_item;
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const int H = p.H, W = p.W;
-  const int64_t HW = (int64_t)H * W;
-  const unsigned total = (unsigned)(p.nframes * p.strips);
-
-  for (;;) {
-    if (threadIdx.x == 0) s_item = atomicAdd(p.work, 1u);
-    __syncthreads();
-    const unsigned item = s_item;
-    __syncthreads();
-    if (item >= total) break;
-    const int64_t frame = item / p.strips;
-    Geo g;
-    item_geometry((int)(item % p.strips), p, warp, g);
-    State S;
-    S.ringw = ((g.p1 - g.p0) + 3) & ~3;
-    S.ring = smem;
-    const float* src = p.in + frame * HW;
-    float* dst = p.out + frame * HW;
-    S.x0 = g.L + 4 * lane;
-    S.lane = lane;
-    S.L = g.L;
-    S.p0 = g.p0;
-    S.p1 = g.p1;
-    S.wring = S.ring + (S.x0 - g.p0);
-    S.rring = S.ring + (min(max(S.x0, g.p0), g.p0 + S.ringw - 4) - g.p0);
-    unsigned incol = 0, needm = 0;
-    S.own = S.outm = S.oob = S.oobL = S.oobR = 0;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int x = S.x0 + c;
-      incol |= (unsigned)(x >= 0 && x < W) << c;
-      S.oobL |= (unsigned)(x < 0) << c;
-      S.oobR |= (unsigned)(x >= W) << c;
-      S.own |= (unsigned)(x >= g.q0 && x < g.q1) << c;
-      S.outm |= (unsigned)(x >= max(g.q0, g.o0) && x < min(g.q1, g.o1)) << c;
-      const bool need = x >= max(max(g.q0 - 2, g.o0 - 2), max(g.p0, 0)) && x < min(min(g.q1 + 2, g.o1 + 2), g.p1);
-      S.nb[c] = need ? -kFMax : kFMax;
-      needm |= (unsigned)need << c;
-    }
-    S.incol = incol;
-    S.full = incol == 0xFu;
-    S.oob = S.oobL | S.oobR;
-    S.woob = __any_sync(kFull, S.oob != 0);
-    S.srcL = (0 - g.L) >> 2;  // lane holding column 0 (component 0)
-    S.srcR = (W - 1 - g.L) >> 2;
-    S.compR = (W - 1 - g.L) & 3;
-    S.srcL = min(max(S.srcL, 0), 31);
-    S.srcR = min(max(S.srcR, 0), 31);
-    S.umax = 0;
-    S.had_empty = S.still_empty = false;
-    S.skip = S.fast = false;
-    S.tmaxN = INT_MAX;
-    set_row(S.ofast, 0.f);
-
-    // ---------------- phase 1 ----------------
-#pragma unroll
-    for (int c = 0; c < 4; ++c) S.T0[c] = INT_MAX, S.top[c] = 0.f;
-    S.tmax = S.tmin = INT_MAX;
-    if (FULL) {
-      phase1<VEC, PRE>(src, p, S.x0, (S.own | needm) != 0, incol, S.T0, S.umax);
-      int mx = INT_MIN, mn = INT_MAX, mxn = INT_MIN;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        if (S.own >> c & 1) {
-          mx = max(mx, S.T0[c]);
-          mn = min(mn, S.T0[c]);
-        }
-        if (needm >> c & 1) mxn = max(mxn, S.T0[c]);
-      }
-      S.tmax = __reduce_max_sync(kFull, mx);
-      S.tmin = __reduce_min_sync(kFull, mn);
-      S.tmaxN = __reduce_max_sync(kFull, mxn);
-    }
-
-    // ---------------- phase 2 ----------------
-#pragma unroll
-    for (int i = 0; i < 2; ++i) set_row(S.c1[i], 0.f), set_row(S.c2[i], 0.f), set_row(S.mprev[i], 0.f);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) set_row(S.c3[i], 0.f), set_row(S.c4[i], kFMax), set_row(S.gc[i], 0.f);
-#pragma unroll
-    for (int i = 0; i < 6; ++i) set_row(S.c5[i], 0.f);
-    S.stg = (uint32_t)__cvta_generic_to_shared(smem + kRing * S.ringw) + warp * (kB * 512) + lane * 16;
-    cp_async_wait_all();  // no copy of the previous item may still land in the slot
-#pragma unroll
-    for (int j = 0; j < kB; ++j)
-      stage_lane<VEC>(S.stg + j * 512, src + (int64_t)(H - 1 - j) * W + S.x0, p.in, j < H, S.full, incol);
-    cp_async_commit();
-    S.lrow = src + (int64_t)(H - 1 - kB) * W + S.x0;
-    S.orow = dst + (int64_t)(H - 1 - (kB * LG::KFirst - LG::C - 2)) * W + S.x0;
-
-    // iterations with every row inside the frame run the lean body
-    const int K = (H + LG::C + 2) / kB + 1;
-    const int kLo = (LG::C + 2 + kB - 1) / kB;  // tc0 - 2 >= 0 and tp >= 0
-    const int kHi = (H - 2 * kB) / kB;           // t0 + 7 <= H - 1 and tc0 + 3 <= H - 1
-    int k = 0;
-    for (; k < min(kLo, K); ++k) iterate<VEC, FULL, BLUR, PRE, DENSE, true>(p, S, k);
-    for (; k <= kHi; ++k) iterate<VEC, FULL, BLUR, PRE, DENSE, false>(p, S, k);
-    for (; k < K; ++k) iterate<VEC, FULL, BLUR, PRE, DENSE, true>(p, S, k);
-
-    // ---------------- per-frame flags ----------------
-    const unsigned um = __reduce_max_sync(kFull, S.umax);
-    const bool he = __any_sync(kFull, S.had_empty);
-    const bool se = __any_sync(kFull, S.still_empty);
-    if (lane == 0) {
-      if (!PRE) atomicMax(p.umax + frame, um);  // PRE: multiscale.cu records it
-      if (FULL && he && p.iters) atomicOr(p.iters + frame, 1);
-      if (FULL && se) {
-        atomicOr(p.status + frame, kNeedsStaged);
-        atomicAdd(p.nfallback, 1ull);
-      }
-    }
-    __syncthreads();  // ring reuse by the next item
-  }
-}
 
 // Per-frame status from the input's largest bit pattern; frames whose max is
 // suspicious (negative sign, non-finite, >= max_depth) are rescanned.
@@ -942,45 +104,11 @@ Layout layout_for(int W, int strips) {
 // strip halos and phase 1 are paid twice).
 Layout layout(int W) { return layout_for(W, W <= kStripMax ? 1 : (W + 1023) / 1024); }
 
-template <int VEC, bool FULL, int BLUR, bool PRE, bool DENSE = false>
-cudaError_t launch_t(const Params& p, size_t smem, int grid, cudaStream_t s) {
-  auto k = fused_kernel<VEC, FULL, BLUR, PRE, DENSE>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  note_launch();
-  k<<<grid, p.nw * 32, smem, s>>>(p);
-  return cudaGetLastError();
-}
-
-template <int VEC, bool FULL>
-cudaError_t dispatch_blur(int blur, bool pre, const Params& p, size_t smem, int grid, cudaStream_t s) {
-  if (pre) {
-    if (blur == DFC_BLUR_GAUSSIAN) return launch_t<VEC, FULL, DFC_BLUR_GAUSSIAN, true>(p, smem, grid, s);
-    if (blur == DFC_BLUR_NONE) return launch_t<VEC, FULL, DFC_BLUR_NONE, true>(p, smem, grid, s);
-    return launch_t<VEC, FULL, kBlurRaw, true>(p, smem, grid, s);
-  }
-  if (blur == DFC_BLUR_GAUSSIAN) return launch_t<VEC, FULL, DFC_BLUR_GAUSSIAN, false>(p, smem, grid, s);
-  if (blur == DFC_BLUR_NONE) return launch_t<VEC, FULL, DFC_BLUR_NONE, false>(p, smem, grid, s);
-  return launch_t<VEC, FULL, kBlurRaw, false>(p, smem, grid, s);
-}
-
-// DENSE (shared-memory scratch for the dense large fill): FULL mode, wide strips, W % 4 == 0
-template <int BLUR>
-cudaError_t dispatch_dense(bool pre, const Params& p, size_t smem, int grid, cudaStream_t s) {
-  return pre ? launch_t<4, true, BLUR, true, true>(p, smem, grid, s) : launch_t<4, true, BLUR, false, true>(p, smem, grid, s);
-}
-
 cudaError_t dispatch(int vec, bool full, int blur, bool pre, const Params& p, size_t smem, int grid, cudaStream_t s) {
-  if (p.dense && vec == 4 && full) {
-    if (blur == DFC_BLUR_GAUSSIAN) return dispatch_dense<DFC_BLUR_GAUSSIAN>(pre, p, smem, grid, s);
-    if (blur == DFC_BLUR_NONE) return dispatch_dense<DFC_BLUR_NONE>(pre, p, smem, grid, s);
-    return dispatch_dense<kBlurRaw>(pre, p, smem, grid, s);
-  }
-  if (vec == 4) return full ? dispatch_blur<4, true>(blur, pre, p, smem, grid, s)
-                            : dispatch_blur<4, false>(blur, pre, p, smem, grid, s);
-  if (vec == 2) return full ? dispatch_blur<2, true>(blur, pre, p, smem, grid, s)
-                            : dispatch_blur<2, false>(blur, pre, p, smem, grid, s);
-  return full ? dispatch_blur<1, true>(blur, pre, p, smem, grid, s) : dispatch_blur<1, false>(blur, pre, p, smem, grid, s);
+  const bool dense = p.dense && vec == 4 && full;
+  if (vec == 4) return fused_dispatch_vec4(full, blur, pre, dense, &p, smem, grid, s);
+  if (vec == 2) return fused_dispatch_vec2(full, blur, pre, false, &p, smem, grid, s);
+  return fused_dispatch_vec1(full, blur, pre, false, &p, smem, grid, s);
 }
 
 }  // namespace

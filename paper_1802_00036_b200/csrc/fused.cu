@@ -178,6 +178,9 @@ cudaError_t launch_fused(const float* in, float* out, int64_t B, int H, int W, c
   p.iters = iters;
   char* w8 = static_cast<char*>(ws);
   p.nfallback = reinterpret_cast<unsigned long long*>(w8);
+#ifdef DFC_TIMING
+  p.tim = reinterpret_cast<unsigned long long*>(getenv("DFC_TIM_PTR") ? strtoull(getenv("DFC_TIM_PTR"), nullptr, 0) : 0);
+#endif
   p.work = reinterpret_cast<unsigned*>(w8 + 8);
   p.umax = reinterpret_cast<unsigned*>(w8 + 16);
   cudaError_t e = cudaMemsetAsync(ws, 0, 16 + (size_t)B * 4, s);

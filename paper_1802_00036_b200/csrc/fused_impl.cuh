@@ -87,6 +87,9 @@ struct Params {
   uint32_t* status;
   int32_t* iters;
   unsigned long long* nfallback;
+#ifdef DFC_TIMING
+  unsigned long long* tim;  // diagnostics build: per (CTA, warp) cycles [producer, barrier, consumer, phase 1]
+#endif
   unsigned* work;
   unsigned* umax;
 };
@@ -374,6 +377,23 @@ __device__ __forceinline__ float lf_hpixel(const float* __restrict__ V, int j, i
 // ---------------------------------------------------------------------------
 // per-item state and one 4-row iteration (EDGE: rows may leave the frame)
 // ---------------------------------------------------------------------------
+// mbarriers replacing the per-block CTA barrier: P[g & 3] completes when every
+// warp has stored block g's stage-5 rows, C[g & 3] when every warp has finished
+// block g's consumer (g counts blocks across items).  A producer overwrites
+// ring slot g mod 10 (rows of block g - 10) only after C[g - 2]: consumers read
+// blocks >= g' - 8 at block g'.  That wait also implies P[g - 4], the newest
+// rows a consumer reads outside the large fill; the large fill waits P[g].
+__device__ __forceinline__ void mb_arrive(uint32_t a) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint32_t a, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+
 struct State {
   const float* rring;  // consumer read base: ring + clamped lane column
   float* wring;        // producer write base: ring + lane column (owned lanes only)
@@ -395,8 +415,13 @@ struct State {
   bool full;           // all 4 columns inside the frame
   unsigned incol;
   float amin;          // FULL: min blurred value (<= 0.1 sends the frame to the staged path)
+#ifdef DFC_TIMING
+  long long tacc[6];   // diagnostics: producer, barrier, consumer, phase 1, consumer LF part, store-only rows
+#endif
   unsigned umax;
   bool had_empty, still_empty;
+  uint32_t mbP, mbC;   // shared addresses of the P[4] / C[4] mbarriers
+  int gk;              // block counter across items (mbarrier index and phase)
   int srcL, srcR, compR;  // replicate sources for out-of-frame columns
 };
 
@@ -407,6 +432,9 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
   const int t0 = kB * k;
   const int tp = t0 - LG::P;
   constexpr int L2 = LG::L2;
+#ifdef DFC_TIMING
+  const long long ta = clock64();
+#endif
   // ======================= producer =======================
   if (FULL && !S.skip && tp > S.tmax) S.skip = true;
   F4 f[kB];
@@ -553,6 +581,8 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
   }
   S.lrow -= kB * W;
   // --- ring store: ring slot of row t is (t + P) mod 40, so this block is slots 4*(k mod 10) + j ---
+  const int g = S.gk++;
+  if (g >= 2) mb_wait(S.mbC + ((g - 2) & 3) * 8, ((g - 2) >> 2) & 1);
   if (S.own) {
     float* w = S.wring + (k % kRingBlocks) * kB * S.ringw;
 #pragma unroll
@@ -560,13 +590,27 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
       if (!EDGE || (tp + j >= 0 && tp + j < H))
         *reinterpret_cast<float4*>(w + j * S.ringw) = make_float4(f[j].v[0], f[j].v[1], f[j].v[2], f[j].v[3]);
   }
-  __syncthreads();
+  __syncwarp();
+  if (S.lane == 0) mb_arrive(S.mbP + (g & 3) * 8);
+#ifdef DFC_TIMING
+  const long long tb = clock64();
+  struct ConsTimer {
+    long long* t;
+    long long tc;
+    __device__ ~ConsTimer() { t[2] += clock64() - tc; }
+  } ct{S.tacc, clock64()};
+  S.tacc[0] += tb - ta;
+#endif
   // ======================= consumer =======================
+  do {
   const int tc0 = t0 - LG::C;
-  if (k < LG::KFirst) return;
+  if (k < LG::KFirst) break;
   float* orow = S.orow;  // output row of processing row tc0 - 2
   S.orow -= kB * W;
   if (FULL && S.fast) {
+#ifdef DFC_TIMING
+    S.tacc[5] += 1;
+#endif
     // every row of the blur windows lies above each needed column's r0: the
     // stage-6 rows are the captured top values and every output row is equal
 #pragma unroll
@@ -575,7 +619,7 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
       if (EDGE && (t < 0 || t >= H)) continue;
       if (S.outm) store_lane<VEC>(orow, S.ofast, S.outm);
     }
-    return;
+    break;
   }
   F4 v6[kB];
   {
@@ -607,6 +651,7 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
         for (int c = 0; c < 4; ++c) em |= (unsigned)!(fmaxf(v6[j].v[c], S.nb[c]) > kValid) << (4 * j + c);
       S.had_empty |= em != 0;
       unsigned lanes = __ballot_sync(kFull, em != 0);
+      mb_wait(S.mbP + (g & 3) * 8, (g >> 2) & 1);  // neighbours' rows up to tc0 + 18
       if (DENSE && __reduce_add_sync(kFull, __popc(em)) > kDenseMin) {
         float* V = S.ring + kRing * S.ringw + p.nw * (kB * 128) + (threadIdx.x >> 5) * (2 * kVC);
 #pragma unroll
@@ -648,6 +693,9 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
       }
     }
   }
+#ifdef DFC_TIMING
+  S.tacc[4] += clock64() - ct.tc;
+#endif
   // out-of-frame columns replicate the edge column (the blur needs true replicate)
   if (S.woob) {
 #pragma unroll
@@ -728,6 +776,9 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
       S.ofast = o;
     }
   }
+  } while (0);
+  __syncwarp();
+  if (S.lane == 0) mb_arrive(S.mbC + (g & 3) * 8);
 }
 
 // ---------------------------------------------------------------------------
@@ -738,8 +789,16 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
   using LG = Lags<PRE>;
   extern __shared__ __align__(16) float smem[];
   __shared__ unsigned s_item;
+  __shared__ __align__(8) unsigned long long s_mb[8];  // P[4], C[4]
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
+  const uint32_t mb0 = (uint32_t)__cvta_generic_to_shared(s_mb);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(mb0 + 8 * i), "r"(p.nw) : "memory");
+  }
+  int gk = 0;  // blocks done across items (mbarrier phases); first use is after the item barrier below
   const int H = p.H, W = p.W;
   const int64_t HW = (int64_t)H * W;
   const unsigned total = (unsigned)(p.nframes * p.strips);
@@ -791,10 +850,17 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
     S.umax = 0;
     S.had_empty = S.still_empty = false;
     S.skip = S.fast = false;
+    S.mbP = mb0;
+    S.mbC = mb0 + 32;
+    S.gk = gk;
     S.tmaxN = INT_MAX;
     set_row(S.ofast, 0.f);
 
     // ---------------- phase 1 ----------------
+#ifdef DFC_TIMING
+    const long long tph = clock64();
+    S.tacc[0] = S.tacc[1] = S.tacc[2] = S.tacc[3] = S.tacc[4] = S.tacc[5] = 0;
+#endif
 #pragma unroll
     for (int c = 0; c < 4; ++c) S.T0[c] = INT_MAX, S.top[c] = 0.f;
     S.tmax = S.tmin = INT_MAX;
@@ -814,6 +880,9 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
       S.tmaxN = __reduce_max_sync(kFull, mxn);
     }
 
+#ifdef DFC_TIMING
+    S.tacc[3] = clock64() - tph;
+#endif
     // ---------------- phase 2 ----------------
 #pragma unroll
     for (int i = 0; i < 2; ++i) set_row(S.c1[i], 0.f), set_row(S.c2[i], 0.f), set_row(S.mprev[i], 0.f);
@@ -839,6 +908,11 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
     for (; k <= kHi; ++k) iterate<VEC, FULL, BLUR, PRE, DENSE, false>(p, S, k);
     for (; k < K; ++k) iterate<VEC, FULL, BLUR, PRE, DENSE, true>(p, S, k);
 
+#ifdef DFC_TIMING
+    if (lane == 0)
+      for (int i = 0; i < 6; ++i) p.tim[(blockIdx.x * kNW + warp) * 6 + i] += S.tacc[i];
+#endif
+    gk = S.gk;
     // ---------------- per-frame flags ----------------
     const unsigned um = __reduce_max_sync(kFull, S.umax);
     const bool he = __any_sync(kFull, S.had_empty);

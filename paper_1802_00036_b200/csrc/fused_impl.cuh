@@ -377,12 +377,15 @@ __device__ __forceinline__ float lf_hpixel(const float* __restrict__ V, int j, i
 // ---------------------------------------------------------------------------
 // per-item state and one 4-row iteration (EDGE: rows may leave the frame)
 // ---------------------------------------------------------------------------
-// mbarriers replacing the per-block CTA barrier: P[g & 3] completes when every
-// warp has stored block g's stage-5 rows, C[g & 3] when every warp has finished
-// block g's consumer (g counts blocks across items).  A producer overwrites
-// ring slot g mod 10 (rows of block g - 10) only after C[g - 2]: consumers read
-// blocks >= g' - 8 at block g'.  That wait also implies P[g - 4], the newest
-// rows a consumer reads outside the large fill; the large fill waits P[g].
+// Per-warp mbarriers (one arrival each) replace the per-block CTA barrier.  A
+// warp's ring columns are read only by itself and its two neighbours (lane
+// halos +-12, large fill +-17 < the 104 owned columns), so warps synchronise
+// with their neighbours only: P_w[g & 3] completes when warp w has stored
+// block g's stage-5 rows, C_w[g & 3] when it has finished block g's consumer
+// (g counts blocks across items).  Warp w overwrites ring slot g mod 10 (rows
+// of block g - 10) after C_{w+-1}[g - 2] (consumers read blocks >= g' - 8 at
+// block g'); that also implies P_{w+-1}[g - 4], the newest rows a consumer
+// reads outside the large fill.  The large fill waits P_{w+-1}[g].
 __device__ __forceinline__ void mb_arrive(uint32_t a) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(a) : "memory");
 }
@@ -420,7 +423,8 @@ struct State {
 #endif
   unsigned umax;
   bool had_empty, still_empty;
-  uint32_t mbP, mbC;   // shared addresses of the P[4] / C[4] mbarriers
+  uint32_t mbW, mbL, mbR;  // shared addresses of this warp's / the neighbours' P[4], C[4] mbarriers
+  bool hasL, hasR;
   int gk;              // block counter across items (mbarrier index and phase)
   int srcL, srcR, compR;  // replicate sources for out-of-frame columns
 };
@@ -582,7 +586,11 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
   S.lrow -= kB * W;
   // --- ring store: ring slot of row t is (t + P) mod 40, so this block is slots 4*(k mod 10) + j ---
   const int g = S.gk++;
-  if (g >= 2) mb_wait(S.mbC + ((g - 2) & 3) * 8, ((g - 2) >> 2) & 1);
+  if (g >= 2) {
+    const uint32_t o = 32 + ((g - 2) & 3) * 8, ph = ((g - 2) >> 2) & 1;
+    if (S.hasL) mb_wait(S.mbL + o, ph);
+    if (S.hasR) mb_wait(S.mbR + o, ph);
+  }
   if (S.own) {
     float* w = S.wring + (k % kRingBlocks) * kB * S.ringw;
 #pragma unroll
@@ -591,7 +599,7 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
         *reinterpret_cast<float4*>(w + j * S.ringw) = make_float4(f[j].v[0], f[j].v[1], f[j].v[2], f[j].v[3]);
   }
   __syncwarp();
-  if (S.lane == 0) mb_arrive(S.mbP + (g & 3) * 8);
+  if (S.lane == 0) mb_arrive(S.mbW + (g & 3) * 8);
 #ifdef DFC_TIMING
   const long long tb = clock64();
   struct ConsTimer {
@@ -651,7 +659,9 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
         for (int c = 0; c < 4; ++c) em |= (unsigned)!(fmaxf(v6[j].v[c], S.nb[c]) > kValid) << (4 * j + c);
       S.had_empty |= em != 0;
       unsigned lanes = __ballot_sync(kFull, em != 0);
-      mb_wait(S.mbP + (g & 3) * 8, (g >> 2) & 1);  // neighbours' rows up to tc0 + 18
+      // neighbours' rows up to tc0 + 18
+      if (S.hasL) mb_wait(S.mbL + (g & 3) * 8, (g >> 2) & 1);
+      if (S.hasR) mb_wait(S.mbR + (g & 3) * 8, (g >> 2) & 1);
       if (DENSE && __reduce_add_sync(kFull, __popc(em)) > kDenseMin) {
         float* V = S.ring + kRing * S.ringw + p.nw * (kB * 128) + (threadIdx.x >> 5) * (2 * kVC);
 #pragma unroll
@@ -778,7 +788,7 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
   }
   } while (0);
   __syncwarp();
-  if (S.lane == 0) mb_arrive(S.mbC + (g & 3) * 8);
+  if (S.lane == 0) mb_arrive(S.mbW + 32 + (g & 3) * 8);
 }
 
 // ---------------------------------------------------------------------------
@@ -789,14 +799,14 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
   using LG = Lags<PRE>;
   extern __shared__ __align__(16) float smem[];
   __shared__ unsigned s_item;
-  __shared__ __align__(8) unsigned long long s_mb[8];  // P[4], C[4]
+  __shared__ __align__(8) unsigned long long s_mb[kNW * 8];  // per warp: P[4], C[4]
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const uint32_t mb0 = (uint32_t)__cvta_generic_to_shared(s_mb);
   if (threadIdx.x == 0) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(mb0 + 8 * i), "r"(p.nw) : "memory");
+    for (int i = 0; i < kNW * 8; ++i)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(mb0 + 8 * i), "r"(1) : "memory");
   }
   int gk = 0;  // blocks done across items (mbarrier phases); first use is after the item barrier below
   const int H = p.H, W = p.W;
@@ -850,8 +860,11 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
     S.umax = 0;
     S.had_empty = S.still_empty = false;
     S.skip = S.fast = false;
-    S.mbP = mb0;
-    S.mbC = mb0 + 32;
+    S.mbW = mb0 + warp * 64;
+    S.mbL = mb0 + (warp - 1) * 64;
+    S.mbR = mb0 + (warp + 1) * 64;
+    S.hasL = warp > 0;
+    S.hasR = warp + 1 < p.nw;
     S.gk = gk;
     S.tmaxN = INT_MAX;
     set_row(S.ofast, 0.f);

@@ -29,6 +29,10 @@
  *   dfc_reimpose              pipeline.py:212-214
  *   dfc_fill_batch            pipeline.py:118-203 (complete / complete_with_stats),
  *                             batched; covers fill_in_fast and fill_in_multiscale
+ *   dfc_fill_batch_raw16      kitti_io.py:36-66 read_depth_png / write_depth_png value
+ *                             conversion fused at the boundary of dfc_fill_batch
+ *   dfc_decode_raw16          kitti_io.py:53 (raw.astype(f32) / f32(256))
+ *   dfc_encode_raw16          kitti_io.py:60-65 (rint(f64(d) * 256) clipped, < 256 m check)
  */
 #ifndef DFC_H_
 #define DFC_H_
@@ -54,6 +58,7 @@ extern "C" {
 #define DFC_ST_NEGATIVE 0x2u    /* ValueError "depth values must be non-negative" (depth_core.py:70-71) */
 #define DFC_ST_DEGENERATE 0x4u  /* DegenerateInputError (pipeline.py:138-140) */
 #define DFC_ST_RANGE 0x8u       /* DepthRangeError (depth_core.py:152-155) */
+#define DFC_ST_ENCODE 0x10u     /* ValueError "depth values must be < 256 m to be encodable" (kitti_io.py:60-61) */
 #define DFC_ST_FALLBACK 0x100u  /* informational: frame was finished by the staged path */
 
 /* kernel shapes (kernels.py:15-19) */
@@ -169,6 +174,22 @@ int dfc_count_empty(const float* in, int64_t B, int32_t H, int32_t W, int64_t* c
 /* out = mask_src > 0.1f ? blurred : 0 */
 int dfc_reimpose(const float* blurred, const float* mask_src, float* out, int64_t B, int32_t H, int32_t W,
                  void* stream);
+
+/* ---- KITTI 16-bit depth PNG values at the boundary ----
+ * raw_in: [B][H][W] uint16, depth = raw / 256 m, raw 0 = empty.
+ * out: float32 depth (out_raw == 0) or uint16 raw (out_raw != 0, rint(depth * 256)
+ * clipped to [0, 65535]; frames with an output >= 256 m get DFC_ST_ENCODE).
+ * Same config, status and iteration semantics as dfc_fill_batch; the fallback
+ * frames are finished inside the call (DFC_F_NO_FINISH is ignored). */
+size_t dfc_workspace_bytes_raw16(const dfc_config* cfg, int64_t B, int32_t H, int32_t W);
+int dfc_fill_batch_raw16(const uint16_t* raw_in, void* out, int32_t out_raw, int64_t B, int32_t H, int32_t W,
+                         const dfc_config* cfg, uint32_t* frame_status, int32_t* large_fill_iters, void* workspace,
+                         size_t ws_bytes, void* stream);
+/* depth = raw / 256 (exact), n elements */
+int dfc_decode_raw16(const uint16_t* raw, float* depth, int64_t n, void* stream);
+/* raw = rint(depth * 256) clipped; frame_status[b] |= DFC_ST_ENCODE if any depth >= 256 (may be NULL) */
+int dfc_encode_raw16(const float* depth, uint16_t* raw, int64_t B, int64_t n_per_frame, uint32_t* frame_status,
+                     void* stream);
 
 #ifdef __cplusplus
 }

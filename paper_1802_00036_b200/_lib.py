@@ -24,6 +24,7 @@ ST_NONFINITE = 0x1
 ST_NEGATIVE = 0x2
 ST_DEGENERATE = 0x4
 ST_RANGE = 0x8
+ST_ENCODE = 0x10
 ST_FALLBACK = 0x100
 
 F_FORCE_STAGED = 0x1
@@ -41,7 +42,7 @@ EXPORTS = (
     "dfc_fill_batch", "dfc_fill_finish", "dfc_op_workspace_bytes", "dfc_box_max", "dfc_box_min",
     "dfc_offsets_max", "dfc_offsets_min", "dfc_median", "dfc_gaussian_separable", "dfc_bilateral",
     "dfc_invert", "dfc_validate", "dfc_masked_fill", "dfc_extend_to_top", "dfc_count_empty",
-    "dfc_reimpose",
+    "dfc_reimpose", "dfc_workspace_bytes_raw16", "dfc_fill_batch_raw16", "dfc_decode_raw16", "dfc_encode_raw16",
 )
 
 
@@ -127,6 +128,10 @@ def load(require: bool = True):
         "dfc_extend_to_top": (ctypes.c_int, [vp, vp, i64, i32, i32, vp]),
         "dfc_count_empty": (ctypes.c_int, [vp, i64, i32, i32, vp, vp]),
         "dfc_reimpose": (ctypes.c_int, [vp, vp, vp, i64, i32, i32, vp]),
+        "dfc_workspace_bytes_raw16": (sz, [cfgp, i64, i32, i32]),
+        "dfc_fill_batch_raw16": (ctypes.c_int, [vp, vp, i32, i64, i32, i32, cfgp, u32p, vp, vp, sz, vp]),
+        "dfc_decode_raw16": (ctypes.c_int, [vp, vp, i64, vp]),
+        "dfc_encode_raw16": (ctypes.c_int, [vp, vp, i64, i64, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

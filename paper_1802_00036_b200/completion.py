@@ -181,6 +181,8 @@ def raise_for_status(status: np.ndarray, max_depth: float) -> None:
         raise DegenerateInputError("input depth map has no valid pixels" + where)
     if s & _lib.ST_RANGE:
         raise DepthRangeError(f"values must be < {max_depth} to be invertible" + where)
+    if s & _lib.ST_ENCODE:  # kitti_io.write_depth_png (kitti_io.py:60-61)
+        raise ValueError("depth values must be < 256 m to be encodable" + where)
 
 
 def _device() -> torch.device:

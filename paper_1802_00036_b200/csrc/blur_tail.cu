@@ -75,9 +75,15 @@ __device__ __forceinline__ float median_at(const float* __restrict__ t, int stri
   return v[(S * S) / 2];
 }
 
-template <int MR, int POST, int PR, bool PARTIAL>
-__global__ void __launch_bounds__(kThreads) blur_tail_kernel(const float* __restrict__ in, float* __restrict__ out,
-                                                             int H, int W, const __grid_constant__ TailParams p) {
+// OUT16: the output is 16-bit KITTI raw, rint(depth * 256) clipped (kitti_io.py:62-65)
+__device__ __forceinline__ unsigned enc_raw16(float v) {
+  return (unsigned)fminf(fmaxf(rintf(v * 256.0f), 0.0f), 65535.0f);
+}
+
+template <int MR, int POST, int PR, bool PARTIAL, bool OUT16>
+__global__ void __launch_bounds__(kThreads) blur_tail_kernel(const float* __restrict__ in, void* __restrict__ out_v,
+                                                             int H, int W, uint32_t* __restrict__ status,
+                                                             const __grid_constant__ TailParams p) {
   constexpr int HI = MR + PR;                      // input halo
   constexpr int kTX = kMW - 2 * PR, kTY = kMH - 2 * PR;
   constexpr int IW = kTX + 2 * HI, IH = kTY + 2 * HI;
@@ -87,7 +93,7 @@ __global__ void __launch_bounds__(kThreads) blur_tail_kernel(const float* __rest
   const int64_t b = blockIdx.z;
   const int x0 = blockIdx.x * kTX, y0 = blockIdx.y * kTY;
   const float* src = in + b * (int64_t)H * W;
-  float* dst = out + b * (int64_t)H * W;
+  bool over = false;  // OUT16: an output >= 256 m
 
   for (int i = threadIdx.x; i < IH * IW; i += kThreads) {
     const int iy = i / IW, ix = i - iy * IW;
@@ -178,28 +184,43 @@ __global__ void __launch_bounds__(kThreads) blur_tail_kernel(const float* __rest
       if (PARTIAL && POST != kPostNone && !(cc[h] > kValid)) o[h] = 0.0f;
       o[h] = o[h] > kValid ? p.md - o[h] : 0.0f;
     }
-    float* q = dst + (int64_t)gy * W + gx;
-    if (gx + 1 < W) {
-      if ((reinterpret_cast<uintptr_t>(q) & 7) == 0)
-        __stcs(reinterpret_cast<float2*>(q), make_float2(o[0], o[1]));
-      else
-        __stcs(q, o[0]), __stcs(q + 1, o[1]);
+    const int64_t off = b * (int64_t)H * W + (int64_t)gy * W + gx;
+    if constexpr (OUT16) {
+      uint16_t* q = static_cast<uint16_t*>(out_v) + off;
+      over |= o[0] >= 256.0f || (gx + 1 < W && o[1] >= 256.0f);
+      if (gx + 1 < W && (reinterpret_cast<uintptr_t>(q) & 3) == 0)
+        __stcs(reinterpret_cast<unsigned*>(q), enc_raw16(o[0]) | enc_raw16(o[1]) << 16);
+      else {
+        q[0] = (uint16_t)enc_raw16(o[0]);
+        if (gx + 1 < W) q[1] = (uint16_t)enc_raw16(o[1]);
+      }
     } else {
-      __stcs(q, o[0]);
+      float* q = static_cast<float*>(out_v) + off;
+      if (gx + 1 < W) {
+        if ((reinterpret_cast<uintptr_t>(q) & 7) == 0)
+          __stcs(reinterpret_cast<float2*>(q), make_float2(o[0], o[1]));
+        else
+          __stcs(q, o[0]), __stcs(q + 1, o[1]);
+      } else {
+        __stcs(q, o[0]);
+      }
     }
   }
+  if (OUT16 && over) atomicOr(status + b, DFC_ST_ENCODE);  // write_depth_png raises (kitti_io.py:60-61)
 }
 
 template <int MR, int POST, int PR>
-cudaError_t launch_t(const float* in, float* out, int64_t B, int H, int W, bool partial, const TailParams& p,
-                     cudaStream_t s) {
+cudaError_t launch_t(const float* in, void* out, int64_t B, int H, int W, bool partial, bool out16, uint32_t* status,
+                     const TailParams& p, cudaStream_t s) {
   constexpr int kTX = kMW - 2 * PR, kTY = kMH - 2 * PR;
   const dim3 grid((W + kTX - 1) / kTX, (H + kTY - 1) / kTY, (unsigned)B);
   note_launch();
   if (partial)
-    blur_tail_kernel<MR, POST, PR, true><<<grid, kThreads, 0, s>>>(in, out, H, W, p);
+    out16 ? blur_tail_kernel<MR, POST, PR, true, true><<<grid, kThreads, 0, s>>>(in, out, H, W, status, p)
+          : blur_tail_kernel<MR, POST, PR, true, false><<<grid, kThreads, 0, s>>>(in, out, H, W, status, p);
   else
-    blur_tail_kernel<MR, POST, PR, false><<<grid, kThreads, 0, s>>>(in, out, H, W, p);
+    out16 ? blur_tail_kernel<MR, POST, PR, false, true><<<grid, kThreads, 0, s>>>(in, out, H, W, status, p)
+          : blur_tail_kernel<MR, POST, PR, false, false><<<grid, kThreads, 0, s>>>(in, out, H, W, status, p);
   return cudaGetLastError();
 }
 
@@ -218,8 +239,8 @@ bool blur_tail_supported(const dfc_config& c) {
 }
 
 // Blur stage + invert back for B frames (in: inverted map; out: direct depth).
-cudaError_t launch_blur_tail(const float* in, float* out, int64_t B, int H, int W, const dfc_config& c,
-                             cudaStream_t s) {
+cudaError_t launch_blur_tail(const float* in, void* out, int64_t B, int H, int W, const dfc_config& c, bool out_raw,
+                             uint32_t* status, cudaStream_t s) {
   const int bm = c.blur_mode;
   const bool med = bm == DFC_BLUR_MEDIAN || bm == DFC_BLUR_MEDIAN_BILATERAL || bm == DFC_BLUR_MEDIAN_GAUSSIAN;
   const bool gauss = bm == DFC_BLUR_GAUSSIAN || bm == DFC_BLUR_MEDIAN_GAUSSIAN;
@@ -250,7 +271,7 @@ cudaError_t launch_blur_tail(const float* in, float* out, int64_t B, int H, int 
   const int mr = med ? c.median_size / 2 : 0;
   const int post = gauss ? kPostGauss : (bil ? kPostBilateral : kPostNone);
 #define DFC_TAIL(MR, POST, PR) \
-  if (mr == MR && post == POST && pr == PR) return launch_t<MR, POST, PR>(in, out, B, H, W, partial, p, s);
+  if (mr == MR && post == POST && pr == PR) return launch_t<MR, POST, PR>(in, out, B, H, W, partial, out_raw, status, p, s);
   DFC_TAIL(0, kPostNone, 0)
   DFC_TAIL(1, kPostNone, 0)
   DFC_TAIL(2, kPostNone, 0)

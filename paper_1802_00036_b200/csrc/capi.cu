@@ -221,7 +221,7 @@ int run_staged(const float* in, float* out, int64_t B, int H, int W, const dfc_c
     }
     // 7 + 8. blur stage (pipeline._blur_stage :206-238) and invert back, one tiled kernel
     if (dfc::blur_tail_supported(c)) {
-      DFC_CK(dfc::launch_blur_tail(cur, y, C, H, W, c, s));
+      DFC_CK(dfc::launch_blur_tail(cur, y, C, H, W, c, false, st, s));
       continue;
     }
     // exact float64 blurs: one op per launch
@@ -517,6 +517,106 @@ int dfc_reimpose(const float* blurred, const float* mask_src, float* out, int64_
   if (rc || B == 0) return rc;
   if (!mask_src) return fail(DFC_E_INVALID, "null buffer");
   DFC_CK(dfc::launch_reimpose(blurred, mask_src, out, B * H * (int64_t)W, as_stream(stream)));
+  return DFC_OK;
+}
+
+// ---- KITTI 16-bit raw at the boundary ------------------------------------
+// Fused path: the fused kernel reads raw rows (and, for Gaussian / no blur,
+// writes raw rows); frames needing more large-fill iterations are decoded one
+// at a time and finished by the staged path.  Other configurations decode a
+// chunk into the workspace, run the float32 pipeline and encode.
+static int64_t raw16_chunk(int64_t B) { return B < 64 ? B : 64; }
+
+size_t dfc_workspace_bytes_raw16(const dfc_config* cfg, int64_t B, int32_t H, int32_t W) {
+  if (!cfg || check_shape(B, H, W) != DFC_OK || check_config(*cfg) != DFC_OK) return 0;
+  const dfc_config c = fit_to_frame(*cfg, H, W);
+  const size_t HW4 = align256((size_t)H * W * 4);
+  if (!(c.flags & DFC_F_FORCE_STAGED) && dfc::fused_supports_raw16(c, H, W))
+    return ws_layout(c, B, H, W).total + 2 * HW4;
+  const int64_t ch = raw16_chunk(B > 0 ? B : 1);
+  return ws_layout(c, ch, H, W).total + 2 * (size_t)ch * HW4;
+}
+
+int dfc_fill_batch_raw16(const uint16_t* raw_in, void* out, int32_t out_raw, int64_t B, int32_t H, int32_t W,
+                         const dfc_config* cfg, uint32_t* frame_status, int32_t* large_fill_iters, void* workspace,
+                         size_t ws_bytes, void* stream) {
+  if (!cfg) return fail(DFC_E_INVALID, "null config");
+  int rc = check_shape(B, H, W);
+  if (rc) return rc;
+  rc = check_config(*cfg);
+  if (rc) return rc;
+  if (B == 0) return DFC_OK;
+  if (!raw_in || !out || !frame_status) return fail(DFC_E_INVALID, "null buffer");
+  const dfc_config c = fit_to_frame(*cfg, H, W);
+  const size_t need = dfc_workspace_bytes_raw16(cfg, B, H, W);
+  if (!workspace || ws_bytes < need)
+    return fail(DFC_E_WORKSPACE, "workspace too small: need " + std::to_string(need) + " bytes");
+  cudaStream_t s = as_stream(stream);
+  const int64_t HW = (int64_t)H * W;
+  const size_t HW4 = align256((size_t)HW * 4);
+  char* ws = static_cast<char*>(workspace);
+  dfc_config cf = c;
+  cf.flags &= ~(uint32_t)DFC_F_NO_FINISH;
+  if (!(c.flags & DFC_F_FORCE_STAGED) && dfc::fused_supports_raw16(c, H, W)) {
+    const WsLayout L = ws_layout(c, B, H, W);
+    float* fin = reinterpret_cast<float*>(ws + L.total);
+    float* fout = reinterpret_cast<float*>(ws + L.total + HW4);
+    DFC_CK(cudaMemsetAsync(frame_status, 0, B * 4, s));
+    if (large_fill_iters) DFC_CK(cudaMemsetAsync(large_fill_iters, 0, B * 4, s));
+    DFC_CK(dfc::launch_fused(raw_in, out, B, H, W, c, frame_status, large_fill_iters, ws, L.fused, s,
+                             out_raw ? 2 : 1));
+    unsigned long long nfb = 0;
+    DFC_CK(cudaMemcpyAsync(&nfb, ws, 8, cudaMemcpyDeviceToHost, s));
+    DFC_CK(cudaStreamSynchronize(s));
+    if (nfb == 0) return DFC_OK;
+    std::vector<uint32_t> st(B);
+    DFC_CK(cudaMemcpyAsync(st.data(), frame_status, B * 4, cudaMemcpyDeviceToHost, s));
+    DFC_CK(cudaStreamSynchronize(s));
+    for (int64_t b = 0; b < B; ++b) {
+      if (!(st[b] & 0x200u)) continue;  // the fused kernel's "needs staged" bit
+      DFC_CK(cudaMemsetAsync(frame_status + b, 0, 4, s));
+      if (large_fill_iters) DFC_CK(cudaMemsetAsync(large_fill_iters + b, 0, 4, s));
+      DFC_CK(dfc::launch_decode_raw16(raw_in + b * HW, fin, HW, s));
+      float* dst = out_raw ? fout : static_cast<float*>(out) + b * HW;
+      rc = run_staged(fin, dst, 1, H, W, c, frame_status + b, large_fill_iters ? large_fill_iters + b : nullptr,
+                      ws + L.fused, L.staged, s);
+      if (rc) return rc;
+      if (out_raw) DFC_CK(dfc::launch_encode_raw16(fout, static_cast<uint16_t*>(out) + b * HW, HW, HW, frame_status + b, s));
+      DFC_CK(dfc::launch_or_status(frame_status + b, DFC_ST_FALLBACK, s));
+    }
+    return DFC_OK;
+  }
+  const int64_t ch = raw16_chunk(B);
+  const size_t inner = ws_layout(c, ch, H, W).total;
+  float* fin = reinterpret_cast<float*>(ws + inner);
+  float* fout = reinterpret_cast<float*>(ws + inner + (size_t)ch * HW4);
+  for (int64_t f0 = 0; f0 < B; f0 += ch) {
+    const int64_t C = B - f0 < ch ? B - f0 : ch;
+    DFC_CK(dfc::launch_decode_raw16(raw_in + f0 * HW, fin, C * HW, s));
+    float* dst = out_raw ? fout : static_cast<float*>(out) + f0 * HW;
+    rc = dfc_fill_batch(fin, dst, C, H, W, &cf, frame_status + f0, large_fill_iters ? large_fill_iters + f0 : nullptr,
+                        ws, inner, stream);
+    if (rc) return rc;
+    if (out_raw)
+      DFC_CK(dfc::launch_encode_raw16(fout, static_cast<uint16_t*>(out) + f0 * HW, HW, C * HW, frame_status + f0, s));
+  }
+  return DFC_OK;
+}
+
+int dfc_decode_raw16(const uint16_t* raw, float* depth, int64_t n, void* stream) {
+  if (n < 0) return fail(DFC_E_INVALID, "negative size");
+  if (n == 0) return DFC_OK;
+  if (!raw || !depth) return fail(DFC_E_INVALID, "null buffer");
+  DFC_CK(dfc::launch_decode_raw16(raw, depth, n, as_stream(stream)));
+  return DFC_OK;
+}
+
+int dfc_encode_raw16(const float* depth, uint16_t* raw, int64_t B, int64_t n_per_frame, uint32_t* frame_status,
+                     void* stream) {
+  if (B < 0 || n_per_frame < 0) return fail(DFC_E_INVALID, "negative size");
+  if (B == 0 || n_per_frame == 0) return DFC_OK;
+  if (!depth || !raw) return fail(DFC_E_INVALID, "null buffer");
+  DFC_CK(dfc::launch_encode_raw16(depth, raw, n_per_frame, B * n_per_frame, frame_status, as_stream(stream)));
   return DFC_OK;
 }
 

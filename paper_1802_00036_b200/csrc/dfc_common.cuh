@@ -77,6 +77,9 @@ cudaError_t launch_validate(const float* in, int64_t n_per_frame, int64_t B, uin
 cudaError_t launch_masked_fill(const float* cur, const float* dil, float* out, int64_t n, cudaStream_t s);
 cudaError_t launch_extend_to_top(const float* in, float* out, int64_t B, int H, int W, cudaStream_t s);
 cudaError_t launch_count_empty(const float* in, int64_t n_per_frame, int64_t B, int64_t* counts, cudaStream_t s);
+cudaError_t launch_decode_raw16(const uint16_t* raw, float* out, int64_t n, cudaStream_t s);
+cudaError_t launch_encode_raw16(const float* in, uint16_t* out, int64_t n_per_frame, int64_t n, uint32_t* status,
+                                cudaStream_t s);
 cudaError_t launch_reimpose(const float* blurred, const float* mask_src, float* out, int64_t n, cudaStream_t s);
 cudaError_t launch_bin_select(const float* direct, const float* inv, float* out, int64_t n, float lo, float hi,
                               cudaStream_t s);
@@ -88,8 +91,8 @@ cudaError_t launch_finalize_status(const int64_t* n_valid, uint32_t* status, int
 
 // ---- blur stage + invert back in one tiled kernel (blur_tail.cu) ---------
 bool blur_tail_supported(const dfc_config& c);
-cudaError_t launch_blur_tail(const float* in, float* out, int64_t B, int H, int W, const dfc_config& c,
-                             cudaStream_t s);
+cudaError_t launch_blur_tail(const float* in, void* out, int64_t B, int H, int W, const dfc_config& c, bool out_raw,
+                             uint32_t* status, cudaStream_t s);
 
 // ---- multiscale stage 1 + 2 (multiscale.cu) -------------------------------
 bool multiscale_stage2_supported(const dfc_config& c);
@@ -100,7 +103,8 @@ cudaError_t launch_multiscale_stage2(const float* in, float* out, int64_t B, int
 struct FusedPlan;
 bool fused_supported(const dfc_config& c, int H, int W);
 size_t fused_workspace_bytes(const dfc_config& c, int64_t B, int H, int W);
-cudaError_t launch_fused(const float* in, float* out, int64_t B, int H, int W, const dfc_config& c,
-                         uint32_t* status, int32_t* iters, void* ws, size_t ws_bytes, cudaStream_t s);
+cudaError_t launch_fused(const void* in, void* out, int64_t B, int H, int W, const dfc_config& c,
+                         uint32_t* status, int32_t* iters, void* ws, size_t ws_bytes, cudaStream_t s, int io = 0);
+bool fused_supports_raw16(const dfc_config& c, int H, int W);
 
 }  // namespace dfc

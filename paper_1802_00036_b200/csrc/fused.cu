@@ -11,15 +11,21 @@ cudaError_t fused_dispatch_vec2(bool full, int blur, bool pre, bool dense, const
                                 cudaStream_t s);
 cudaError_t fused_dispatch_vec1(bool full, int blur, bool pre, bool dense, const void* params, size_t smem, int grid,
                                 cudaStream_t s);
+cudaError_t fused_dispatch_raw16(int io, bool full, int blur, const void* params, size_t smem, int grid, cudaStream_t s);
 
 namespace {
 
 // Per-frame status from the input's largest bit pattern; frames whose max is
 // suspicious (negative sign, non-finite, >= max_depth) are rescanned.
 __global__ void finalize_kernel(const float* __restrict__ in, int64_t HW, const unsigned* __restrict__ umax,
-                                uint32_t* status, float md) {
+                                uint32_t* status, float md, bool in_raw) {
   const int64_t b = blockIdx.x;
   const unsigned u = umax[b];
+  if (in_raw) {  // raw / 256 is finite and >= 0: the max decides RANGE and DEGENERATE alone
+    if (threadIdx.x == 0 && u >= __float_as_uint(md)) atomicOr(status + b, DFC_ST_RANGE);
+    if (threadIdx.x == 0 && u <= __float_as_uint(kValid)) atomicOr(status + b, DFC_ST_DEGENERATE);
+    return;
+  }
   if (u < __float_as_uint(md)) {
     if (u <= __float_as_uint(kValid) && threadIdx.x == 0) atomicOr(status + b, DFC_ST_DEGENERATE);
     return;
@@ -104,7 +110,9 @@ Layout layout_for(int W, int strips) {
 // strip halos and phase 1 are paid twice).
 Layout layout(int W) { return layout_for(W, W <= kStripMax ? 1 : (W + 1023) / 1024); }
 
-cudaError_t dispatch(int vec, bool full, int blur, bool pre, const Params& p, size_t smem, int grid, cudaStream_t s) {
+cudaError_t dispatch(int vec, bool full, int blur, bool pre, int io, const Params& p, size_t smem, int grid,
+                     cudaStream_t s) {
+  if (io) return fused_dispatch_raw16(io, full, blur, &p, smem, grid, s);  // vec 4, no PRE (fused_supports_raw16)
   const bool dense = p.dense && vec == 4 && full;
   if (vec == 4) return fused_dispatch_vec4(full, blur, pre, dense, &p, smem, grid, s);
   if (vec == 2) return fused_dispatch_vec2(full, blur, pre, false, &p, smem, grid, s);
@@ -150,8 +158,16 @@ size_t fused_workspace_bytes(const dfc_config& c, int64_t B, int H, int W) {
   return raw_offset(B) + (raw_mode(c) ? a : 0) + (c.multiscale ? a : 0) + 256;
 }
 
-cudaError_t launch_fused(const float* in, float* out, int64_t B, int H, int W, const dfc_config& c,
-                         uint32_t* status, int32_t* iters, void* ws, size_t ws_bytes, cudaStream_t s) {
+bool fused_supports_raw16(const dfc_config& c, int H, int W) {
+  return fused_supported(c, H, W) && W % 4 == 0 && !c.multiscale;
+}
+
+// io 0: float32 in / out; 1: 16-bit KITTI raw in, float32 out; 2: raw in / raw out
+cudaError_t launch_fused(const void* in_v, void* out_v, int64_t B, int H, int W, const dfc_config& c,
+                         uint32_t* status, int32_t* iters, void* ws, size_t ws_bytes, cudaStream_t s, int io) {
+  const float* in = static_cast<const float*>(in_v);  // io 0; raw pointers below go through in_v / out_v
+  float* out = static_cast<float*>(out_v);
+  const size_t isz = io ? 2 : 4, osz = io == 2 ? 2 : 4;
   if (ws_bytes < fused_workspace_bytes(c, B, H, W)) return cudaErrorInvalidValue;
   Params p;
   p.in = in;
@@ -216,8 +232,9 @@ cudaError_t launch_fused(const float* in, float* out, int64_t B, int H, int W, c
     const int64_t C = B - f0 < chunk ? B - f0 : chunk;
     if (pre && (e = launch_multiscale_stage2(in + f0 * HW, s2, C, H, W, c, op, on, umax0 + f0, s)) != cudaSuccess)
       return e;
-    p.in = pre ? s2 : in + f0 * HW;
-    p.out = raw ? tmp : out + f0 * HW;
+    char* out_c = static_cast<char*>(out_v) + f0 * HW * osz;
+    p.in = pre ? (const void*)s2 : (const void*)(static_cast<const char*>(in_v) + f0 * HW * isz);
+    p.out = raw ? (void*)tmp : (void*)out_c;
     p.nframes = C;
     p.status = status + f0;
     p.iters = iters ? iters + f0 : nullptr;
@@ -226,12 +243,13 @@ cudaError_t launch_fused(const float* in, float* out, int64_t B, int H, int W, c
     const int64_t items = C * L.strips;
     const int64_t slots = (int64_t)sms * L.per_sm;
     const int grid = (int)(items < slots ? items : slots);
-    e = dispatch(vec, full, blur, pre, p, L.smem, grid, s);
+    // raw mode: the fused kernel writes float32 stage-6 maps; the blur tail encodes
+    e = dispatch(vec, full, blur, pre, raw && io == 2 ? 1 : io, p, L.smem, grid, s);
     if (e != cudaSuccess) return e;
-    if (raw && (e = launch_blur_tail(tmp, out + f0 * HW, C, H, W, c, s)) != cudaSuccess) return e;
+    if (raw && (e = launch_blur_tail(tmp, out_c, C, H, W, c, io == 2, status + f0, s)) != cudaSuccess) return e;
   }
   note_launch();
-  finalize_kernel<<<(unsigned)B, 256, 0, s>>>(in, HW, umax0, status, c.max_depth);
+  finalize_kernel<<<(unsigned)B, 256, 0, s>>>(in, HW, umax0, status, c.max_depth, io != 0);
   return cudaGetLastError();
 }
 

@@ -75,9 +75,28 @@ constexpr int64_t kRawChunk = 296;     // frames per fused -> blur-tail round (2
 static_assert(kRing % kB == 0 && kLag % kB == 0, "ring blocks must not wrap inside a block");
 
 
+// Element types at the boundary.  IO 0: float32 depth in / out; 1: KITTI
+// 16-bit raw in (depth = raw / 256, kitti_io.py:53) / float32 out; 2: raw in /
+// raw out (rint(depth * 256) clipped, kitti_io.py:62-65).
+template <int IO>
+struct IoT {
+  using In = float;
+  using Out = float;
+};
+template <>
+struct IoT<1> {
+  using In = uint16_t;
+  using Out = float;
+};
+template <>
+struct IoT<2> {
+  using In = uint16_t;
+  using Out = uint16_t;
+};
+
 struct Params {
-  const float* in;
-  float* out;
+  const void* in;
+  void* out;
   int64_t nframes;
   int dense;  // shared-memory scratch for the dense large fill is available
   int H, W, strips, SW, nw;
@@ -107,22 +126,30 @@ __device__ __forceinline__ void cp_async_zfill(uint32_t sdst, const void* gsrc, 
 }
 
 template <int VEC>
-__device__ __forceinline__ void stage_lane(uint32_t sdst, const float* q, const float* safe, bool rowok, bool full,
+__device__ __forceinline__ void stage_lane(uint32_t sdst, const uint16_t* q, const void* safe, bool rowok, bool full,
+                                           unsigned incol) {
+  static_assert(VEC == 4, "16-bit input is staged 8 bytes per lane (W % 4 == 0)");
+  const bool ok = rowok && full;
+  cp_async_zfill<8>(sdst, ok ? (const void*)q : safe, ok);
+}
+
+template <int VEC>
+__device__ __forceinline__ void stage_lane(uint32_t sdst, const float* q, const void* safe, bool rowok, bool full,
                                            unsigned incol) {
   if constexpr (VEC == 4) {
     const bool ok = rowok && full;
-    cp_async_zfill<16>(sdst, ok ? q : safe, ok);
+    cp_async_zfill<16>(sdst, ok ? (const void*)q : safe, ok);
   } else if constexpr (VEC == 2) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const bool ok = rowok && ((incol >> (2 * h)) & 3u) == 3u;
-      cp_async_zfill<8>(sdst + 8 * h, ok ? q + 2 * h : safe, ok);
+      cp_async_zfill<8>(sdst + 8 * h, ok ? (const void*)(q + 2 * h) : safe, ok);
     }
   } else {
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const bool ok = rowok && (incol >> c & 1);
-      cp_async_zfill<4>(sdst + 4 * c, ok ? q + c : safe, ok);
+      cp_async_zfill<4>(sdst + 4 * c, ok ? (const void*)(q + c) : safe, ok);
     }
   }
 }
@@ -135,6 +162,66 @@ __device__ __forceinline__ F4 lds4(uint32_t saddr) {
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n" : "=f"(q.x), "=f"(q.y), "=f"(q.z), "=f"(q.w) : "r"(saddr)
                : "memory");
   return F4{{q.x, q.y, q.z, q.w}};
+}
+
+// raw / 256 is exact in float32 for every 16-bit raw value (kitti_io.py:53)
+__device__ __forceinline__ float raw_m(unsigned r) { return (float)r * 0.00390625f; }
+
+__device__ __forceinline__ F4 unpack_raw(unsigned a, unsigned b) {
+  return F4{{raw_m(a & 0xFFFFu), raw_m(a >> 16), raw_m(b & 0xFFFFu), raw_m(b >> 16)}};
+}
+
+template <typename T>
+__device__ __forceinline__ F4 lds4_t(uint32_t saddr) {
+  if constexpr (sizeof(T) == 4) {
+    return lds4(saddr);
+  } else {
+    unsigned a, b;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];\n" : "=r"(a), "=r"(b) : "r"(saddr) : "memory");
+    return unpack_raw(a, b);
+  }
+}
+
+// one lane's 4 columns of a row, bounds-checked (phase 1)
+template <int VEC, typename T>
+__device__ __forceinline__ F4 load4_t(const T* row, int x0, int W) {
+  if constexpr (sizeof(T) == 4) {
+    return load4<VEC, false>(row, x0, W);
+  } else {
+    if (x0 >= 0 && x0 + 3 < W) {
+      const uint2 u = __ldg(reinterpret_cast<const uint2*>(row + x0));
+      return unpack_raw(u.x, u.y);
+    }
+    F4 r;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) r.v[c] = (x0 + c >= 0 && x0 + c < W) ? raw_m(__ldg(row + x0 + c)) : 0.0f;
+    return r;
+  }
+}
+
+// rint(depth * 256) clipped to [0, 65535] (kitti_io.py:62-65); depth * 256 is
+// exact, so round-to-nearest-even here equals numpy's float64 rint
+__device__ __forceinline__ unsigned enc_raw(float v) {
+  const float r = rintf(v * 256.0f);
+  return (unsigned)fminf(fmaxf(r, 0.0f), 65535.0f);
+}
+
+template <int VEC, typename T>
+__device__ __forceinline__ void store_lane_t(T* q, const F4& a, unsigned colmask, bool& over) {
+  if constexpr (sizeof(T) == 4) {
+    store_lane<VEC>(q, a, colmask);
+  } else {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) over |= (colmask >> c & 1u) && a.v[c] >= 256.0f;  // write_depth_png raises
+    if (colmask == 0xFu) {
+      const uint2 u = make_uint2(enc_raw(a.v[0]) | enc_raw(a.v[1]) << 16, enc_raw(a.v[2]) | enc_raw(a.v[3]) << 16);
+      __stcs(reinterpret_cast<uint2*>(q), u);
+    } else {
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (colmask >> c & 1u) q[c] = (uint16_t)enc_raw(a.v[c]);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -177,8 +264,8 @@ __device__ void item_geometry(int s, const Params& p, int warp, Geo& g) {
 // ---------------------------------------------------------------------------
 // bit i of w[c]: (inverted) validity of row y0 + i; PRE: the frame is the
 // stage-2 map in the inverted encoding already
-template <int VEC, bool PRE>
-__device__ __forceinline__ void load_bits(const float* frame, int H, int W, int x0, int y0, float md, uint32_t w[4],
+template <int VEC, bool PRE, typename T>
+__device__ __forceinline__ void load_bits(const T* frame, int H, int W, int x0, int y0, float md, uint32_t w[4],
                                           unsigned& umax) {
 #pragma unroll
   for (int c = 0; c < 4; ++c) w[c] = 0;
@@ -190,7 +277,7 @@ __device__ __forceinline__ void load_bits(const float* frame, int H, int W, int 
     for (int i = 0; i < 16; ++i) {
       const int y = y0 + 16 * h + i;
       if (y < H)
-        v[i] = load4<VEC, false>(frame + (int64_t)y * W, x0, W);
+        v[i] = load4_t<VEC>(frame + (int64_t)y * W, x0, W);
       else
         set_row(v[i], 0.f);
     }
@@ -240,13 +327,13 @@ __device__ __forceinline__ void hcomb(const uint64_t in[4], uint64_t out[4]) {
   }
 }
 
-template <int VEC, bool PRE>
-__device__ __forceinline__ void phase1(const float* frame, const Params& p, int x0, bool needed, unsigned incol,
+template <int VEC, bool PRE, typename T>
+__device__ __forceinline__ void phase1(const T* frame, const Params& p, int x0, bool needed, unsigned incol,
                                        int T0[4], unsigned& umax) {
   const int H = p.H, W = p.W;
   uint32_t prv[4] = {0, 0, 0, 0}, cur[4], nxt[4];
   load_bits<VEC, PRE>(frame, H, W, x0, 0, p.md, cur, umax);
-  load_bits<VEC, PRE>(frame, H, W, x0, 32, p.md, nxt, umax);
+  load_bits<VEC, PRE>(frame, H, W, x0, 32, p.md, nxt, umax);  // (T deduced)
   int r0[4] = {-1, -1, -1, -1};
   uint64_t cm[4];
 #pragma unroll
@@ -413,8 +500,9 @@ struct State {
   F4 c1[2], c2[2], c3[4], c4[4], c5[6], gc[4], mprev[2];
   F4 ofast;            // output row above every needed r0 (FULL): all such rows are equal
   uint32_t stg;        // shared-memory staging slot of this lane (row j at +512 j)
-  const float* lrow;   // input row of processing row t0 + kB at column x0
-  float* orow;         // output row of processing row tc0 - 2 at column x0
+  const void* lrow;    // input row of processing row t0 + kB at column x0
+  void* orow;          // output row of processing row tc0 - 2 at column x0
+  bool enc_over;       // IO 2: an output >= 256 m (not encodable)
   bool full;           // all 4 columns inside the frame
   unsigned incol;
   float amin;          // FULL: min blurred value (<= 0.1 sends the frame to the staged path)
@@ -429,8 +517,10 @@ struct State {
   int srcL, srcR, compR;  // replicate sources for out-of-frame columns
 };
 
-template <int VEC, bool FULL, int BLUR, bool PRE, bool DENSE, bool EDGE>
+template <int VEC, bool FULL, int BLUR, bool PRE, bool DENSE, int IO, bool EDGE>
 __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
+  using TIn = typename IoT<IO>::In;
+  using TOut = typename IoT<IO>::Out;
   using LG = Lags<PRE>;
   const int H = p.H, W = p.W;
   const int t0 = kB * k;
@@ -447,7 +537,7 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
     cp_async_wait_all();  // this block's rows, staged one block ago
 #pragma unroll
     for (int j = 0; j < kB; ++j) {
-      a[j] = lds4(S.stg + j * 512);
+      a[j] = lds4_t<TIn>(S.stg + j * 512);
       if constexpr (!PRE) {
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -468,7 +558,7 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
       asm volatile("" ::"r"(S.umax));
     }
     if (!FULL || (t0 + kB - LG::P <= S.tmax)) {
-      const float* q = S.lrow;
+      const TIn* q = static_cast<const TIn*>(S.lrow);
 #pragma unroll
       for (int j = 0; j < kB; ++j, q -= W)
         stage_lane<VEC>(S.stg + j * 512, q, p.in, !EDGE || t0 + kB + j < H, S.full, S.incol);
@@ -583,7 +673,7 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
 #pragma unroll
       for (int c = 0; c < 4; ++c) f[j].v[c] = S.top[c];
   }
-  S.lrow -= kB * W;
+  S.lrow = static_cast<const TIn*>(S.lrow) - kB * W;
   // --- ring store: ring slot of row t is (t + P) mod 40, so this block is slots 4*(k mod 10) + j ---
   const int g = S.gk++;
   if (g >= 2) {
@@ -613,8 +703,8 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
   do {
   const int tc0 = t0 - LG::C;
   if (k < LG::KFirst) break;
-  float* orow = S.orow;  // output row of processing row tc0 - 2
-  S.orow -= kB * W;
+  TOut* orow = static_cast<TOut*>(S.orow);  // output row of processing row tc0 - 2
+  S.orow = orow - kB * W;
   if (FULL && S.fast) {
 #ifdef DFC_TIMING
     S.tacc[5] += 1;
@@ -625,7 +715,7 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
     for (int j = 0; j < kB; ++j, orow -= W) {
       const int t = tc0 - 2 + j;
       if (EDGE && (t < 0 || t >= H)) continue;
-      if (S.outm) store_lane<VEC>(orow, S.ofast, S.outm);
+      if (S.outm) store_lane_t<VEC>(orow, S.ofast, S.outm, S.enc_over);
     }
     break;
   }
@@ -762,7 +852,7 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
         if (!FULL && !(mk[j].v[c] > kValid)) o.v[c] = 0.0f;
         if (!FULL && !(mk[j].v[c + 1] > kValid)) o.v[c + 1] = 0.0f;
       }
-      if (S.outm) store_lane<VEC>(orow, o, S.outm);
+      if (S.outm) store_lane_t<VEC>(orow, o, S.outm, S.enc_over);
     }
     // rows tc0-4 .. tc0+3 above every needed r0: output row tc0+1 repeats from here on
     if (FULL && !EDGE && tc0 - 4 > S.tmaxN) {
@@ -779,7 +869,7 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
 #pragma unroll
       for (int c = 0; c < 4; ++c)
         o.v[c] = BLUR == kBlurRaw ? v6[j].v[c] : (v6[j].v[c] > kValid ? p.md - v6[j].v[c] : 0.0f);
-      if (S.outm) store_lane<VEC>(orow, o, S.outm);
+      if (S.outm) store_lane_t<VEC>(orow, o, S.outm, S.enc_over);
     }
     if (FULL && !EDGE && tc0 > S.tmaxN) {
       S.fast = true;
@@ -794,8 +884,10 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
 // ---------------------------------------------------------------------------
 // the fused kernel
 // ---------------------------------------------------------------------------
-template <int VEC, bool FULL, int BLUR, bool PRE, bool DENSE>
+template <int VEC, bool FULL, int BLUR, bool PRE, bool DENSE, int IO>
 __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constant__ Params p) {
+  using TIn = typename IoT<IO>::In;
+  using TOut = typename IoT<IO>::Out;
   using LG = Lags<PRE>;
   extern __shared__ __align__(16) float smem[];
   __shared__ unsigned s_item;
@@ -825,8 +917,8 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
     State S;
     S.ringw = ((g.p1 - g.p0) + 3) & ~3;
     S.ring = smem;
-    const float* src = p.in + frame * HW;
-    float* dst = p.out + frame * HW;
+    const TIn* src = static_cast<const TIn*>(p.in) + frame * HW;
+    TOut* dst = static_cast<TOut*>(p.out) + frame * HW;
     S.x0 = g.L + 4 * lane;
     S.lane = lane;
     S.L = g.L;
@@ -859,7 +951,7 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
     S.srcR = min(max(S.srcR, 0), 31);
     S.umax = 0;
     S.had_empty = S.still_empty = false;
-    S.skip = S.fast = false;
+    S.skip = S.fast = S.enc_over = false;
     S.mbW = mb0 + warp * 64;
     S.mbL = mb0 + (warp - 1) * 64;
     S.mbR = mb0 + (warp + 1) * 64;
@@ -917,9 +1009,9 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
     const int kLo = (LG::C + 2 + kB - 1) / kB;  // tc0 - 2 >= 0 and tp >= 0
     const int kHi = (H - 2 * kB) / kB;           // t0 + 7 <= H - 1 and tc0 + 3 <= H - 1
     int k = 0;
-    for (; k < min(kLo, K); ++k) iterate<VEC, FULL, BLUR, PRE, DENSE, true>(p, S, k);
-    for (; k <= kHi; ++k) iterate<VEC, FULL, BLUR, PRE, DENSE, false>(p, S, k);
-    for (; k < K; ++k) iterate<VEC, FULL, BLUR, PRE, DENSE, true>(p, S, k);
+    for (; k < min(kLo, K); ++k) iterate<VEC, FULL, BLUR, PRE, DENSE, IO, true>(p, S, k);
+    for (; k <= kHi; ++k) iterate<VEC, FULL, BLUR, PRE, DENSE, IO, false>(p, S, k);
+    for (; k < K; ++k) iterate<VEC, FULL, BLUR, PRE, DENSE, IO, true>(p, S, k);
 
 #ifdef DFC_TIMING
     if (lane == 0)
@@ -930,8 +1022,10 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
     const unsigned um = __reduce_max_sync(kFull, S.umax);
     const bool he = __any_sync(kFull, S.had_empty);
     const bool se = __any_sync(kFull, S.still_empty);
+    const bool eo = IO == 2 && __any_sync(kFull, S.enc_over);
     if (lane == 0) {
       if (!PRE) atomicMax(p.umax + frame, um);  // PRE: multiscale.cu records it
+      if (eo) atomicOr(p.status + frame, DFC_ST_ENCODE);
       if (FULL && he && p.iters) atomicOr(p.iters + frame, 1);
       if (FULL && se) {
         atomicOr(p.status + frame, kNeedsStaged);
@@ -942,9 +1036,9 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
   }
 }
 
-template <int VEC, bool FULL, int BLUR, bool PRE, bool DENSE = false>
+template <int VEC, bool FULL, int BLUR, bool PRE, bool DENSE = false, int IO = 0>
 cudaError_t launch_t(const Params& p, size_t smem, int grid, cudaStream_t s) {
-  auto k = fused_kernel<VEC, FULL, BLUR, PRE, DENSE>;
+  auto k = fused_kernel<VEC, FULL, BLUR, PRE, DENSE, IO>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   note_launch();

@@ -607,6 +607,36 @@ cudaError_t launch_extend_to_top(const float* in, float* out, int64_t B, int H, 
   return cudaGetLastError();
 }
 
+namespace {
+__global__ void decode_raw16_kernel(const uint16_t* __restrict__ raw, float* __restrict__ out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (float)raw[i] * 0.00390625f;  // exact (kitti_io.py:53)
+}
+
+__global__ void encode_raw16_kernel(const float* __restrict__ in, uint16_t* __restrict__ out, int64_t n_per_frame,
+                                    int64_t n, uint32_t* status) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = in[i];
+    // np.rint(f64(v) * 256) clipped (kitti_io.py:64-65); v * 256 is exact in float32
+    out[i] = (uint16_t)fminf(fmaxf(rintf(v * 256.0f), 0.0f), 65535.0f);
+    if (status && v >= 256.0f) atomicOr(status + i / n_per_frame, DFC_ST_ENCODE);
+  }
+}
+}  // namespace
+
+cudaError_t launch_decode_raw16(const uint16_t* raw, float* out, int64_t n, cudaStream_t s) {
+  note_launch();
+  decode_raw16_kernel<<<grid1d(n), 256, 0, s>>>(raw, out, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_encode_raw16(const float* in, uint16_t* out, int64_t n_per_frame, int64_t n, uint32_t* status,
+                                cudaStream_t s) {
+  note_launch();
+  encode_raw16_kernel<<<grid1d(n), 256, 0, s>>>(in, out, n_per_frame, n, status);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_reimpose(const float* blurred, const float* mask_src, float* out, int64_t n, cudaStream_t s) {
   note_launch();
   reimpose_kernel<<<grid1d(n), 256, 0, s>>>(blurred, mask_src, out, n);

@@ -222,3 +222,51 @@ def fill_batch(frames: torch.Tensor, cfg: "_lib.DfcConfig", out: torch.Tensor | 
     check(L.dfc_fill_batch(_ptr(x), _ptr(out), B, H, W, ctypes.byref(cfg), _ptr(status), _ptr(iterations),
                            _ptr(ws), ws.numel(), _stream()))
     return FillResult(out, status, iterations)
+
+
+# ---------------------------------------------------------------------------
+# KITTI 16-bit raw at the boundary (kitti_io.py:36-66)
+# ---------------------------------------------------------------------------
+
+def fill_batch_raw16(raw: torch.Tensor, cfg: "_lib.DfcConfig", out_raw: bool = True,
+                     workspace: Workspace | None = None) -> FillResult:
+    """dfc_fill_batch_raw16: uint16 raw frames in; uint16 raw (or float32 depth) out."""
+    if raw.dtype != torch.uint16:
+        raise TypeError("raw frames must be torch.uint16")
+    x = raw.contiguous()
+    if x.dim() == 2:
+        x = x.unsqueeze(0)
+    B, H, W = x.shape
+    L = _lib.load()
+    need = int(L.dfc_workspace_bytes_raw16(ctypes.byref(cfg), B, H, W))
+    if need == 0:
+        check(L.dfc_fill_batch_raw16(None, None, int(out_raw), B, H, W, ctypes.byref(cfg), None, None, None, 0,
+                                     _stream()))
+    if workspace is None:
+        workspace = _default_ws.setdefault(x.device, Workspace())
+    ws = workspace.get(need, x.device)
+    out = torch.empty(x.shape, dtype=torch.uint16 if out_raw else torch.float32, device=x.device)
+    status = torch.empty(B, dtype=torch.int32, device=x.device)
+    iterations = torch.empty(B, dtype=torch.int32, device=x.device)
+    check(L.dfc_fill_batch_raw16(_ptr(x), _ptr(out), int(out_raw), B, H, W, ctypes.byref(cfg), _ptr(status),
+                                 _ptr(iterations), _ptr(ws), ws.numel(), _stream()))
+    return FillResult(out, status, iterations)
+
+
+def decode_raw16(raw: torch.Tensor) -> torch.Tensor:
+    """depth = raw / 256 (kitti_io.py:53), exact."""
+    x = raw.contiguous()
+    out = torch.empty(x.shape, dtype=torch.float32, device=x.device)
+    check(_lib.load().dfc_decode_raw16(_ptr(x), _ptr(out), x.numel(), _stream()))
+    return out
+
+
+def encode_raw16(depth: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+    """raw = rint(depth * 256) clipped (kitti_io.py:62-65); per-frame status (DFC_ST_ENCODE if any >= 256 m)."""
+    x, _ = _as_batch(depth)
+    B = x.shape[0]
+    out = torch.empty(x.shape, dtype=torch.uint16, device=x.device)
+    status = torch.zeros(B, dtype=torch.int32, device=x.device)
+    check(_lib.load().dfc_encode_raw16(_ptr(x), _ptr(out), B, x[0].numel(), _ptr(status), _stream()))
+    return out.reshape(depth.shape), status
+

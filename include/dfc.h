@@ -33,6 +33,8 @@
  *                             conversion fused at the boundary of dfc_fill_batch
  *   dfc_decode_raw16          kitti_io.py:53 (raw.astype(f32) / f32(256))
  *   dfc_encode_raw16          kitti_io.py:60-65 (rint(f64(d) * 256) clipped, < 256 m check)
+ *   dfc_error_sums            metrics.py:119-137 (_error_sums, per frame; MetricsAccumulator sums them)
+ *   dfc_error_map             metrics.py:101-108 (error_map)
  */
 #ifndef DFC_H_
 #define DFC_H_
@@ -190,6 +192,15 @@ int dfc_decode_raw16(const uint16_t* raw, float* depth, int64_t n, void* stream)
 /* raw = rint(depth * 256) clipped; frame_status[b] |= DFC_ST_ENCODE if any depth >= 256 (may be NULL) */
 int dfc_encode_raw16(const float* depth, uint16_t* raw, int64_t B, int64_t n_per_frame, uint32_t* frame_status,
                      void* stream);
+
+/* ---- error metrics vs ground truth ----
+ * Over pixels where pred and gt are both > 0.1f: sums[b][0..3] (device, float64) =
+ * sum err^2, sum |err|, sum (1/d - 1/g)^2, sum |1/d - 1/g| (err = d - g, meters);
+ * counts[b][0] = such pixels, counts[b][1] = gt-valid pixels left empty by pred. */
+int dfc_error_sums(const float* pred, const float* gt, int64_t B, int32_t H, int32_t W, double* sums, int64_t* counts,
+                   void* stream);
+/* out = |f64(pred) - f64(gt)| (float32) where both are valid, else 0 */
+int dfc_error_map(const float* pred, const float* gt, float* out, int64_t B, int32_t H, int32_t W, void* stream);
 
 #ifdef __cplusplus
 }

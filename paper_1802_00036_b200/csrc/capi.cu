@@ -620,4 +620,23 @@ int dfc_encode_raw16(const float* depth, uint16_t* raw, int64_t B, int64_t n_per
   return DFC_OK;
 }
 
+int dfc_error_sums(const float* pred, const float* gt, int64_t B, int32_t H, int32_t W, double* sums, int64_t* counts,
+                   void* stream) {
+  int rc = check_shape(B, H, W);
+  if (rc) return rc;
+  if (B == 0) return DFC_OK;
+  if (!pred || !gt || !sums || !counts) return fail(DFC_E_INVALID, "null buffer");
+  DFC_CK(dfc::launch_error_sums(pred, gt, B, (int64_t)H * W, sums, counts, as_stream(stream)));
+  return DFC_OK;
+}
+
+int dfc_error_map(const float* pred, const float* gt, float* out, int64_t B, int32_t H, int32_t W, void* stream) {
+  int rc = check_shape(B, H, W);
+  if (rc) return rc;
+  if (B == 0) return DFC_OK;
+  if (!pred || !gt || !out) return fail(DFC_E_INVALID, "null buffer");
+  DFC_CK(dfc::launch_error_map(pred, gt, out, B * H * (int64_t)W, as_stream(stream)));
+  return DFC_OK;
+}
+
 }  // extern "C"

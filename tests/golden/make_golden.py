@@ -13,10 +13,17 @@ and stores its outputs:
                             reference output bytes (inputs are regenerated
                             from their seeds and also hashed),
 * ``multiscale_small.npz`` -- the composed multiscale oracle built from the
-                            reference's own morphology.dilate per depth bin.
+                            reference's own morphology.dilate per depth bin,
+* ``metrics_small.npz`` / ``metrics_small.json`` -- metrics.evaluate, error_map
+                            and MetricsAccumulator on seeded prediction / ground
+                            truth pairs,
+* ``kitti_small.npz``    -- kitti_io.write_depth_png -> read_depth_png on
+                            seeded maps through real 16-bit PNG files (written
+                            to a scratch directory inside the repo, removed).
 
 Nothing here is copied from a dataset; every input is generated from a seed.
-Usage:  python tests/golden/make_golden.py   (needs /root/reference)
+Usage:  python tests/golden/make_golden.py [name ...]   (needs /root/reference;
+        names: ops stages pipeline multiscale full metrics kitti; default all)
 """
 
 from __future__ import annotations
@@ -291,10 +298,67 @@ def gen_multiscale():
     (HERE / "multiscale_small.json").write_text(json.dumps(meta, indent=1))
 
 
+def gen_metrics():
+    from depthfill import metrics
+
+    rng = np.random.default_rng(2024)
+    out, meta = {}, []
+    acc = metrics.MetricsAccumulator()
+    for k, (h, w) in enumerate([(1, 1), (3, 5), (17, 31), (64, 80), (120, 300)]):
+        gt = rand_map(rng, h, w, p_empty=0.6)
+        pred = gt + rng.normal(0, 0.5, size=gt.shape).astype(np.float32)
+        pred = np.where(rng.random(gt.shape) < 0.2, np.float32(0.0), np.abs(pred)).astype(np.float32)
+        pred[0, 0] = gt[0, 0] = np.float32(5.0)  # at least one shared valid pixel
+        p = depth_core.DepthMap(pred)
+        g = depth_core.DepthMap(gt)
+        rep = metrics.evaluate(p, g)
+        acc.add(p, g)
+        out[f"pred_{k}"] = pred
+        out[f"gt_{k}"] = gt
+        out[f"emap_{k}"] = metrics.error_map(p, g)
+        meta.append({"key": k, "sums": list(metrics._error_sums(p, g)), "report": [
+            rep.rmse_mm, rep.mae_mm, rep.irmse_invkm, rep.imae_invkm, rep.evaluated_pixels, rep.skipped_pixels]})
+    r = acc.finalize()
+    meta.append({"accumulated": [r.rmse_mm, r.mae_mm, r.irmse_invkm, r.imae_invkm, r.evaluated_pixels,
+                                 r.skipped_pixels]})
+    np.savez_compressed(HERE / "metrics_small.npz", **out)
+    (HERE / "metrics_small.json").write_text(json.dumps(meta, indent=1))
+
+
+def gen_kitti():
+    import shutil
+
+    from depthfill import kitti_io
+
+    rng = np.random.default_rng(99)
+    tmp = ROOT / "gpurun_out" / "_golden_png"
+    tmp.mkdir(parents=True, exist_ok=True)
+    out = {}
+    try:
+        for k, (h, w) in enumerate([(1, 1), (7, 9), (40, 64)]):
+            v = rng.uniform(0.0, 255.99, size=(h, w)).astype(np.float32)
+            v[rng.random((h, w)) < 0.3] = 0.0
+            v.flat[0] = np.float32(1.5 / 256.0)  # an exact tie (raw 1.5 -> 2)
+            path = tmp / f"k{k}.png"
+            kitti_io.write_depth_png(depth_core.DepthMap(v), path)
+            back = kitti_io.read_depth_png(path).values
+            out[f"in_{k}"] = v
+            out[f"back_{k}"] = np.array(back)
+        raw = np.arange(65536, dtype=np.uint16).reshape(256, 256)
+        path = tmp / "all.png"
+        from PIL import Image
+
+        Image.fromarray(raw).save(path)
+        out["all_raw_decoded"] = np.array(kitti_io.read_depth_png(path).values)
+    finally:
+        shutil.rmtree(tmp, ignore_errors=True)
+    np.savez_compressed(HERE / "kitti_small.npz", **out)
+
+
+GENS = {"ops": gen_ops, "stages": gen_stages, "pipeline": gen_pipeline_small, "multiscale": gen_multiscale,
+        "full": gen_pipeline_full, "metrics": gen_metrics, "kitti": gen_kitti}
+
 if __name__ == "__main__":
-    gen_ops()
-    gen_stages()
-    gen_pipeline_small()
-    gen_multiscale()
-    gen_pipeline_full()
+    for name in sys.argv[1:] or list(GENS):
+        GENS[name]()
     print("golden vectors written to", HERE)

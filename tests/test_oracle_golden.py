@@ -125,3 +125,35 @@ def test_pipeline_full_golden(golden_dir, case):
     dense, info = O.complete_with_stats(v, _cfg(meta["cfg"], meta["offset"]))
     assert hashlib.sha256(dense.tobytes()).hexdigest() == meta["output_sha256"]
     assert info["large_fill_iterations"] == meta["iters"]
+
+
+def test_metrics_oracle_matches_reference(golden_dir):
+    """oracle/metrics_oracle.py against depthfill.metrics outputs."""
+    from oracle import metrics_oracle as M
+
+    z = np.load(golden_dir / "metrics_small.npz")
+    meta = json.loads((golden_dir / "metrics_small.json").read_text())
+    tot = np.zeros(4)
+    n = s = 0
+    for m in meta[:-1]:
+        k = m["key"]
+        sums = M.error_sums(z[f"pred_{k}"], z[f"gt_{k}"])
+        assert list(sums) == m["sums"]
+        assert list(M.finalize(*sums)) == m["report"]
+        assert np.array_equal(M.error_map(z[f"pred_{k}"], z[f"gt_{k}"]), z[f"emap_{k}"])
+        tot += np.array(sums[:4])
+        n += sums[4]
+        s += sums[5]
+    assert list(M.finalize(*tot, n, s)) == meta[-1]["accumulated"]
+
+
+def test_kitti_oracle_matches_reference_png_roundtrip(golden_dir):
+    """decode / encode against kitti_io.write_depth_png -> read_depth_png through real PNG files."""
+    from oracle import metrics_oracle as M
+
+    z = np.load(golden_dir / "kitti_small.npz")
+    for k in range(3):
+        back = M.decode_raw16(M.encode_raw16(z[f"in_{k}"]))
+        assert np.array_equal(back.view(np.uint32), z[f"back_{k}"].view(np.uint32))
+    raw = np.arange(65536, dtype=np.uint16).reshape(256, 256)
+    assert np.array_equal(M.decode_raw16(raw).view(np.uint32), z["all_raw_decoded"].view(np.uint32))

@@ -150,12 +150,17 @@ int64_t round_frames(const dfc_config& c, int64_t B, int W) {
   return B < ch ? B : ch;
 }
 
+size_t t0_bytes(const dfc_config& c, int64_t B, int W) {
+  return c.fill_mode == DFC_FILL_FULL ? (((size_t)round_frames(c, B, W) * W * 4 + 255) & ~(size_t)255) : 0;
+}
+
 size_t fused_workspace_bytes(const dfc_config& c, int64_t B, int H, int W) {
   // [0] u64 frames needing the staged path, [8] u32 work counter, [16..) u32 umax[B],
-  // then one round of stage-6 maps (raw mode) and of stage-2 maps (multiscale)
+  // then one round of stage-6 maps (raw mode), of stage-2 maps (multiscale) and
+  // of per-column r0 rows (FULL)
   const size_t map = (size_t)round_frames(c, B, W) * H * W * 4;
   const size_t a = (map + 255) & ~(size_t)255;
-  return raw_offset(B) + (raw_mode(c) ? a : 0) + (c.multiscale ? a : 0) + 256;
+  return raw_offset(B) + (raw_mode(c) ? a : 0) + (c.multiscale ? a : 0) + t0_bytes(c, B, W) + 256;
 }
 
 bool fused_supports_raw16(const dfc_config& c, int H, int W) {
@@ -214,6 +219,7 @@ cudaError_t launch_fused(const void* in_v, void* out_v, int64_t B, int H, int W,
   const size_t map = (((size_t)chunk * HW * 4) + 255) & ~(size_t)255;
   float* tmp = raw ? reinterpret_cast<float*>(w8 + raw_offset(B)) : nullptr;
   float* s2 = pre ? reinterpret_cast<float*>(w8 + raw_offset(B) + (raw ? map : 0)) : nullptr;
+  p.t0g = full ? reinterpret_cast<int32_t*>(w8 + raw_offset(B) + (raw ? map : 0) + (pre ? map : 0)) : nullptr;
   unsigned* umax0 = p.umax;
   std::vector<int32_t> offs[3];
   const int32_t* op[3];

@@ -99,6 +99,7 @@ struct Params {
   void* out;
   int64_t nframes;
   int dense;  // shared-memory scratch for the dense large fill is available
+  int32_t* t0g;  // FULL: per-column r0 row (processing order) from r0_kernel, [nframes][W]
   int H, W, strips, SW, nw;
   float md;
   float gw[5];
@@ -970,7 +971,10 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
     for (int c = 0; c < 4; ++c) S.T0[c] = INT_MAX, S.top[c] = 0.f;
     S.tmax = S.tmin = INT_MAX;
     if (FULL) {
-      phase1<VEC, PRE>(src, p, S.x0, (S.own | needm) != 0, incol, S.T0, S.umax);
+      // phase 1 ran in r0_kernel for the whole round (latency-bound scans overlap there)
+      const int32_t* tr = p.t0g + frame * W + S.x0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) S.T0[c] = (incol >> c & 1) ? __ldg(tr + c) : INT_MAX;
       int mx = INT_MIN, mn = INT_MAX, mxn = INT_MIN;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -1036,8 +1040,50 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
   }
 }
 
+// Phase 1 of every (item, warp slot) of a round as independent warps (the
+// fused kernel's geometry): each warp finds its owned columns' r0 rows and
+// records the largest input bit pattern of the rows it scanned (the top rows,
+// which phase 2 does not read).  One 32-row block costs a global-load round
+// trip; many warps per SM hide it, which the fused kernel's 12 could not.
+template <int VEC, bool PRE, int IO>
+__global__ void __launch_bounds__(128) r0_kernel(const __grid_constant__ Params p) {
+  using TIn = typename IoT<IO>::In;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (gw >= p.nframes * p.strips * p.nw) return;  // whole warp
+  const int64_t item = gw / p.nw;
+  const int64_t frame = item / p.strips;
+  Geo g;
+  item_geometry((int)(item % p.strips), p, (int)(gw % p.nw), g);
+  const int x0 = g.L + 4 * lane;
+  unsigned incol = 0, own = 0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int x = x0 + c;
+    incol |= (unsigned)(x >= 0 && x < p.W) << c;
+    own |= (unsigned)(x >= g.q0 && x < g.q1) << c;
+  }
+  const TIn* src = static_cast<const TIn*>(p.in) + frame * (int64_t)p.H * p.W;
+  int T0[4];
+  unsigned umax = 0;
+  phase1<VEC, PRE>(src, p, x0, own != 0, incol, T0, umax);
+  int32_t* dst = p.t0g + frame * p.W + x0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    if (own >> c & 1) dst[c] = T0[c];
+  if (!PRE) {
+    umax = __reduce_max_sync(kFull, umax);
+    if (lane == 0) atomicMax(p.umax + frame, umax);
+  }
+}
+
 template <int VEC, bool FULL, int BLUR, bool PRE, bool DENSE = false, int IO = 0>
 cudaError_t launch_t(const Params& p, size_t smem, int grid, cudaStream_t s) {
+  if constexpr (FULL) {
+    const int64_t warps = p.nframes * p.strips * p.nw;
+    note_launch();
+    r0_kernel<VEC, PRE, IO><<<(unsigned)((warps + 3) / 4), 128, 0, s>>>(p);
+  }
   auto k = fused_kernel<VEC, FULL, BLUR, PRE, DENSE, IO>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

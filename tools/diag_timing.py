@@ -66,17 +66,16 @@ def run(frames=1024):
         assert rc == 0, rc
         torch.cuda.synchronize()
     t = tim.view(148, 12, 6).cpu().numpy().astype(np.float64)
-    print("store-only consumer iterations per warp:", t[:, :, 5].mean())
-    t = t[:, :, :5]
-    names = ["producer", "barrier", "consumer", "phase1", "(cons: ring+LF)"]
-    tot = t[:, :, :4].sum(axis=2)
+    names = ["producer", "(C wait)", "consumer", "phase1", "(cons:ring+LF)", "(LF wait)"]
+    tot = t[:, :, [0, 2, 3]].sum(axis=2)
     print("per-warp mean cycles (over CTAs), share of warp time:")
     print("warp " + " ".join(f"{n:>10s}" for n in names) + "      total")
     for w in range(12):
         m = t[:, w, :].mean(axis=0)
         print(f"{w:4d} " + " ".join(f"{v / 1e6:9.2f}M" for v in m) + f" {tot[:, w].mean() / 1e6:9.2f}M")
     allm = t.sum(axis=(0, 1))
-    print("all  " + " ".join(f"{v / allm[:4].sum() * 100:9.1f}%" for v in allm))
+    print("all  " + " ".join(f"{v / allm[[0, 2, 3]].sum() * 100:9.1f}%" for v in allm))
+    print("(parenthesised columns are parts of the producer / consumer columns)")
 
 
 if __name__ == "__main__":

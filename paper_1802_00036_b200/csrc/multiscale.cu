@@ -106,17 +106,95 @@ __device__ __forceinline__ F4 cross3(const F4& up, const F4& mid, const F4& dn) 
 
 // one cross3 stage over a 4-row block with 2 carried rows; zeroes rows outside
 // [0, H) (row of output j: t0 - lag + j) and out-of-frame columns
+template <bool EDGE, bool WOOB>
 __device__ __forceinline__ void cross3_block(F4 carry[2], const F4 in4[kB], F4 out[kB], int row0, int H,
-                                             unsigned oob, bool edge_rows) {
+                                             unsigned oob) {
   const F4 in[kB + 2] = {carry[0], carry[1], in4[0], in4[1], in4[2], in4[3]};
 #pragma unroll
   for (int j = 0; j < kB; ++j) {
     out[j] = cross3(in[j], in[j + 1], in[j + 2]);
-    if (edge_rows && (row0 + j < 0 || row0 + j >= H)) set_row(out[j], 0.f);
-    fix_oob(out[j], oob, 0.f);
+    if (EDGE && (row0 + j < 0 || row0 + j >= H)) set_row(out[j], 0.f);
+    if (WOOB) fix_oob(out[j], oob, 0.f);
   }
   carry[0] = in4[2];
   carry[1] = in4[3];
+}
+
+struct MsState {
+  F4 nc[6], m1[2], m2[2], m3[2], f1[2], f2[2], fd, nx[kB];
+  unsigned um;
+};
+
+// one 4-row block: input rows t0..t0+3 in, output rows t0-3..t0 out.  EDGE:
+// rows may lie outside the frame; WOOB: the warp has out-of-frame columns.
+template <int VEC, bool EDGE, bool WOOB>
+__device__ __forceinline__ void ms_block(MsState& S, const float* __restrict__ src, float* __restrict__ dst, int t0,
+                                         int H, int W, int x0, unsigned oob, unsigned own, const MsFastParams& p) {
+  F4 cur[kB];
+#pragma unroll
+  for (int j = 0; j < kB; ++j) {
+    cur[j] = S.nx[j];
+    if (!EDGE || t0 + kB + j < H)
+      S.nx[j] = load4<VEC, true>(src + (int64_t)(t0 + kB + j) * W, x0, W);
+    else
+      set_row(S.nx[j], 0.f);
+  }
+  F4 nv[kB], mv[kB], fv[kB];
+#pragma unroll
+  for (int j = 0; j < kB; ++j)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const float v = cur[j].v[c];
+      S.um = max(S.um, __float_as_uint(v));
+      const float inv = v > kValid ? p.md - v : 0.0f;  // depth_core.invert
+      const bool near = v <= p.edge_near, far = v > p.edge_far;
+      nv[j].v[c] = near ? inv : 0.0f;
+      fv[j].v[c] = far ? inv : 0.0f;
+      mv[j].v[c] = (near || far) ? 0.0f : inv;
+    }
+  // near: FULL7 box (rows t0-3+j)
+  F4 nb[kB];
+  {
+    const F4 col[kB + 6] = {S.nc[0], S.nc[1], S.nc[2], S.nc[3], S.nc[4], S.nc[5], nv[0], nv[1], nv[2], nv[3]};
+    F4 vv[kB];
+    vwin3<OpMax>(col, vv);
+#pragma unroll
+    for (int j = 0; j < kB; ++j) nb[j] = hwin3<OpMax>(ext_row<3>(vv[j]));
+    S.nc[0] = S.nc[4], S.nc[1] = S.nc[5];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) S.nc[i + 2] = nv[i];
+  }
+  // medium: DIAMOND7 = cross3^3 (rows t0-1+j, t0-2+j, t0-3+j)
+  F4 a1[kB], a2[kB], a3[kB];
+  cross3_block<EDGE, WOOB>(S.m1, mv, a1, t0 - 1, H, oob);
+  cross3_block<EDGE, WOOB>(S.m2, a1, a2, t0 - 2, H, oob);
+  cross3_block<EDGE, WOOB>(S.m3, a2, a3, t0 - 3, H, oob);
+  // far: DIAMOND5 = cross3^2 (rows t0-2+j), delayed one row
+  F4 b1[kB], b2[kB];
+  cross3_block<EDGE, WOOB>(S.f1, fv, b1, t0 - 1, H, oob);
+  cross3_block<EDGE, WOOB>(S.f2, b1, b2, t0 - 2, H, oob);
+  const F4 fr[kB] = {S.fd, b2[0], b2[1], b2[2]};
+  S.fd = b2[3];
+#pragma unroll
+  for (int j = 0; j < kB; ++j) {
+    const int y = t0 - 3 + j;
+    if (EDGE && (y < 0 || y >= H)) continue;
+    F4 o;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) o.v[c] = fmx3(nb[j].v[c], a3[j].v[c], fr[j].v[c]);
+    if (own) store4<VEC>(dst + (int64_t)y * W, x0, o, own);
+  }
+}
+
+template <int VEC, bool WOOB>
+__device__ __forceinline__ void ms_rows(MsState& S, const float* src, float* dst, int H, int W, int x0, unsigned oob,
+                                        unsigned own, const MsFastParams& p) {
+  // the lean body needs every row it touches inside the frame: stages and
+  // outputs down to t0 - 3 (t0 >= 4), the prefetch up to t0 + 7 (t0 + 8 <= H)
+  int t0 = 0;
+  for (; t0 < 4 && t0 < H + 3; t0 += kB) ms_block<VEC, true, WOOB>(S, src, dst, t0, H, W, x0, oob, own, p);
+  for (; t0 + 2 * kB <= H; t0 += kB) ms_block<VEC, false, WOOB>(S, src, dst, t0, H, W, x0, oob, own, p);
+  for (; t0 < H + 3; t0 += kB) ms_block<VEC, true, WOOB>(S, src, dst, t0, H, W, x0, oob, own, p);
 }
 
 template <int VEC>
@@ -137,81 +215,26 @@ __global__ void __launch_bounds__(kMsWarps * 32) ms_fast_kernel(const float* __r
     oob |= (unsigned)(x < 0 || x >= W) << c;
     own |= (unsigned)(lane >= 1 && lane <= 30 && x < W) << c;
   }
-  F4 nc[6], m1[2], m2[2], m3[2], f1[2], f2[2], fd;
+  MsState S;
 #pragma unroll
-  for (int i = 0; i < 6; ++i) set_row(nc[i], 0.f);
+  for (int i = 0; i < 6; ++i) set_row(S.nc[i], 0.f);
 #pragma unroll
-  for (int i = 0; i < 2; ++i) set_row(m1[i], 0.f), set_row(m2[i], 0.f), set_row(m3[i], 0.f), set_row(f1[i], 0.f),
-      set_row(f2[i], 0.f);
-  set_row(fd, 0.f);
-  unsigned um = 0;
-  F4 nx[kB];  // next block's input rows, loaded one block ahead
+  for (int i = 0; i < 2; ++i)
+    set_row(S.m1[i], 0.f), set_row(S.m2[i], 0.f), set_row(S.m3[i], 0.f), set_row(S.f1[i], 0.f), set_row(S.f2[i], 0.f);
+  set_row(S.fd, 0.f);
+  S.um = 0;
 #pragma unroll
   for (int j = 0; j < kB; ++j) {
     if (j < H)
-      nx[j] = load4<VEC, true>(src + (int64_t)j * W, x0, W);
+      S.nx[j] = load4<VEC, true>(src + (int64_t)j * W, x0, W);
     else
-      set_row(nx[j], 0.f);
+      set_row(S.nx[j], 0.f);
   }
-  for (int t0 = 0; t0 < H + 3; t0 += kB) {
-    const bool edge_rows = t0 < 3 || t0 + kB > H;
-    F4 cur[kB];
-#pragma unroll
-    for (int j = 0; j < kB; ++j) {
-      cur[j] = nx[j];
-      if (t0 + kB + j < H)
-        nx[j] = load4<VEC, true>(src + (int64_t)(t0 + kB + j) * W, x0, W);
-      else
-        set_row(nx[j], 0.f);
-    }
-    F4 nv[kB], mv[kB], fv[kB];
-#pragma unroll
-    for (int j = 0; j < kB; ++j) {
-      const F4 d = cur[j];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const float v = d.v[c];
-        um = max(um, __float_as_uint(v));
-        const float inv = v > kValid ? p.md - v : 0.0f;  // depth_core.invert
-        nv[j].v[c] = v <= p.edge_near ? inv : 0.0f;
-        mv[j].v[c] = (v > p.edge_near && v <= p.edge_far) ? inv : 0.0f;
-        fv[j].v[c] = v > p.edge_far ? inv : 0.0f;
-      }
-    }
-    // near: FULL7 box (rows t0-3+j)
-    F4 nb[kB];
-    {
-      const F4 col[kB + 6] = {nc[0], nc[1], nc[2], nc[3], nc[4], nc[5], nv[0], nv[1], nv[2], nv[3]};
-      F4 vv[kB];
-      vwin3<OpMax>(col, vv);
-#pragma unroll
-      for (int j = 0; j < kB; ++j) nb[j] = hwin3<OpMax>(ext_row<3>(vv[j]));
-      nc[0] = nc[4], nc[1] = nc[5];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) nc[i + 2] = nv[i];
-    }
-    // medium: DIAMOND7 = cross3^3 (rows t0-1+j, t0-2+j, t0-3+j)
-    F4 a1[kB], a2[kB], a3[kB];
-    cross3_block(m1, mv, a1, t0 - 1, H, oob, edge_rows);
-    cross3_block(m2, a1, a2, t0 - 2, H, oob, edge_rows);
-    cross3_block(m3, a2, a3, t0 - 3, H, oob, edge_rows);
-    // far: DIAMOND5 = cross3^2 (rows t0-2+j), delayed one row
-    F4 b1[kB], b2[kB];
-    cross3_block(f1, fv, b1, t0 - 1, H, oob, edge_rows);
-    cross3_block(f2, b1, b2, t0 - 2, H, oob, edge_rows);
-    const F4 fr[kB] = {fd, b2[0], b2[1], b2[2]};
-    fd = b2[3];
-#pragma unroll
-    for (int j = 0; j < kB; ++j) {
-      const int y = t0 - 3 + j;
-      if (y < 0 || y >= H) continue;
-      F4 o;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) o.v[c] = fmx3(nb[j].v[c], a3[j].v[c], fr[j].v[c]);
-      store4<VEC>(dst + (int64_t)y * W, x0, o, own);
-    }
-  }
-  um = __reduce_max_sync(kFull, um);
+  if (__any_sync(kFull, oob != 0))
+    ms_rows<VEC, true>(S, src, dst, H, W, x0, oob, own, p);
+  else
+    ms_rows<VEC, false>(S, src, dst, H, W, x0, oob, own, p);
+  const unsigned um = __reduce_max_sync(kFull, S.um);
   if (lane == 0) atomicMax(umax + b, um);
 }
 

@@ -5,13 +5,13 @@
 // (pipeline._blur_stage, pipeline.py:206-238; morphology.py:99-125;
 // depth_core.invert_back :150-156.)  Input: the stage-6 (FULL) or stage-4
 // (PARTIAL) map in the inverted encoding; output: the final direct-depth map.
-// One CTA per output tile (64 x 32 minus the blur halo): the input tile (+
+// One CTA per output tile (64 x 64 minus the blur halo): the input tile (+
 // median and blur halos, replicate-clamped) is staged in shared memory, the
 // median is computed on the tile plus the blur halo -- each halo position
 // outside the frame at its frame-clamped centre, which is exactly the
 // replicate border the reference's blur sees -- then the blur, re-impose and
 // re-inversion run two pixels per thread.  The 5x5 median uses one shared
-// min/max network per 4x2 block of outputs (median_block.cuh, ~70 min/max per
+// min/max network per 8x2 block of outputs (median_block.cuh, ~64 min/max per
 // output instead of ~200 for a separate median-of-25 network).
 //
 // The median is exact (selection network, bit-identical to the reference's
@@ -31,9 +31,9 @@
 namespace dfc {
 namespace {
 
-// The median region (output tile + blur halo) is kMW x kMH = 64 x 32: 256
-// blocks of 4 x 2 medians, one per thread.  Output tile = region - 2 PR.
-constexpr int kMW = 64, kMH = 32, kThreads = 256;
+// The median region (output tile + blur halo) is kMW x kMH = 64 x 64: 256
+// blocks of 8 x 2 medians, one per thread.  Output tile = region - 2 PR.
+constexpr int kMW = 64, kMH = 64, kThreads = 256;
 static_assert((kMW / kMedBlockW) * (kMH / kMedBlockH) == kThreads, "one median block per thread");
 constexpr int kPostNone = 0, kPostGauss = 1, kPostBilateral = 2;
 
@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(kThreads) blur_tail_kernel(const float* __rest
 
   // stage-7a: median (or copy) on the tile + blur halo, at frame-clamped centres
   if constexpr (MR == 2) {
-    // shared 4x2-block network on the regular grid; positions outside the
+    // shared 8x2-block network on the regular grid; positions outside the
     // frame then take the value at their clamped position
     const int bx = threadIdx.x % (MW / kMedBlockW), by = threadIdx.x / (MW / kMedBlockW);
     const int mx = bx * kMedBlockW, my = by * kMedBlockH;

@@ -195,7 +195,7 @@ def emit(TW, TH):
 
 
 def main():
-    TW, TH = 4, 2
+    TW, TH = (int(v) for v in sys.argv[1:3]) if len(sys.argv) >= 3 else (8, 2)
     n, body = emit(TW, TH)
     text = [
         "// GENERATED by tools/gen_median_blocks.py -- do not edit.",

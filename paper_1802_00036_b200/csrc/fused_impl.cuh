@@ -1046,7 +1046,7 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
 // which phase 2 does not read).  One 32-row block costs a global-load round
 // trip; many warps per SM hide it, which the fused kernel's 12 could not.
 template <int VEC, bool PRE, int IO>
-__global__ void __launch_bounds__(128) r0_kernel(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(128, 4) r0_kernel(const __grid_constant__ Params p) {
   using TIn = typename IoT<IO>::In;
   const int lane = threadIdx.x & 31;
   const int64_t gw = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);

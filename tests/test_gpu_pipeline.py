@@ -379,3 +379,47 @@ def test_wide_sparse_frames_dense_large_fill(P, blur):
         ref, info = O.complete_with_stats(frames[i], _ocfg(kw))
         _cmp(got[i], ref, blur)
         assert int(res.iterations[i]) == info["large_fill_iterations"]
+
+
+def _rand_case(rng):
+    h, w = int(rng.integers(16, 160)), int(rng.integers(16, 700))
+    spec = synth.SynthSpec(width=w, height=h, beams=int(rng.integers(4, max(5, min(64, h // 2)))),
+                           density=(float(rng.uniform(0.005, 0.05)),) * 2,
+                           max_depth=float(rng.choice([100.0, 120.0, 60.0])))
+    blur = str(rng.choice(["none", "gaussian", "median", "bilateral", "median_gaussian", "median_bilateral"]))
+    fill = str(rng.choice(["full", "partial"]))
+    shape = str(rng.choice(["diamond", "full", "cross", "circle"]))
+    size = int(rng.choice([3, 5, 7]))
+    multi = bool(rng.random() < 0.3)
+    return spec, blur, fill, shape, size, multi
+
+
+@pytest.mark.parametrize("case", range(100))
+def test_randomized_configs_vs_oracle(P, case):
+    """Seeded random shapes, densities, max_depth, blur / fill modes, stage-2 kernels
+    and multiscale bins: every device path (fused, raw + blur tail, PRE, staged) vs the oracle."""
+    rng = np.random.default_rng(10_000 + case)
+    spec, blur, fill, shape, size, multi = _rand_case(rng)
+    frames = np.stack([synth.make_frame(spec, [1234, case, i]) for i in range(2)])
+    kw = {"blur_mode": blur, "fill_mode": fill}
+    md = spec.max_depth
+    if multi:
+        ms = P.MultiscaleConfig(near=(P.KernelShape(shape), size))
+        res = P.complete_batch(frames, _pcfg(P, kw, offset=md), multiscale=ms, raise_on_error=False)
+        ocfg = O.OracleConfig(**{**_ocfg(kw, md).__dict__, "multiscale": (
+            (15.0, 30.0), (O.KernelShape(shape), size), (O.KernelShape.DIAMOND, 7), (O.KernelShape.DIAMOND, 5))})
+    else:
+        kw2 = {**kw, "dilation_shape": shape, "dilation_size": size}
+        res = P.complete_batch(frames, _pcfg(P, kw2, offset=md), raise_on_error=False)
+        ocfg = _ocfg(kw2, md)
+    got = res.dense.cpu().numpy()
+    st = res.status.cpu().numpy()
+    for i in range(frames.shape[0]):
+        try:
+            ref, info = O.complete_with_stats(frames[i], ocfg)
+        except Exception as e:  # the reference raises: the device must flag the frame
+            assert st[i] & 0xFF, (type(e).__name__, st[i])
+            continue
+        assert not st[i] & 0xFF, st[i]
+        _cmp(got[i], ref, blur)
+        assert int(res.iterations[i]) == info["large_fill_iterations"]

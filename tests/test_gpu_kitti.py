@@ -63,7 +63,7 @@ def _pcfg(P, kw):
     return P.PipelineConfig(**{k: conv[k](x) if k in conv else x for k, x in kw.items()})
 
 
-@pytest.mark.parametrize("shape", [(352, 1216), (375, 1242), (64, 300)])
+@pytest.mark.parametrize("shape", [(352, 1216), (375, 1242), (64, 300), (96, 2600)])
 @pytest.mark.parametrize("blur,fill", [("none", "full"), ("gaussian", "full"), ("median_bilateral", "full"),
                                        ("bilateral", "partial"), ("none", "partial")])
 def test_raw16_pipeline_vs_oracle(K, shape, blur, fill):

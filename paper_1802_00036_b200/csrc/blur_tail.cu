@@ -163,11 +163,13 @@ __global__ void __launch_bounds__(kThreads) blur_tail_kernel(const float* __rest
         }
       r = __fadd2_rn(c, a);
     } else if constexpr (POST == kPostBilateral) {
-      float2 acc = make_float2(0.f, 0.f), den = make_float2(0.f, 0.f);
+      // the centre tap has d = 0 and weight exactly 1 (ex2(0))
+      float2 acc = make_float2(0.f, 0.f), den = make_float2(1.f, 1.f);
 #pragma unroll
       for (int dy = 0; dy <= 2 * PR; ++dy)
 #pragma unroll
         for (int dx = 0; dx <= 2 * PR; ++dx) {
+          if (dy == PR && dx == PR) continue;
           const float2 d = __fadd2_rn(make_float2(m[dy * MW + dx], m[dy * MW + dx + 1]), make_float2(-c.x, -c.y));
           const float ks = p.ks[dy * (2 * PR + 1) + dx];
           const float2 e = __ffma2_rn(__fmul2_rn(make_float2(p.kv, p.kv), d), d, make_float2(ks, ks));

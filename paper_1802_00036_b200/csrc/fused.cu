@@ -99,8 +99,8 @@ Layout layout_for(int W, int strips) {
   L.smem = (size_t)kRing * ringw * 4 + (size_t)L.nw * kB * 512;
   // dense large-fill scratch when it fits next to the ring (wide strips; a
   // whole 1216-wide frame's ring leaves no room -- its empties are sparse)
-  L.dense = L.smem + (size_t)L.nw * 2 * kVC * 4 <= kSmemMax;
-  if (L.dense) L.smem += (size_t)L.nw * 2 * kVC * 4;
+  L.dense = L.smem + (size_t)L.nw * kB * kVC * 4 <= kSmemMax;
+  if (L.dense) L.smem += (size_t)L.nw * kB * kVC * 4;
   L.per_sm = 1;
   return L;
 }

@@ -412,19 +412,21 @@ __device__ __forceinline__ float lf_one(const float* __restrict__ ring, int ring
   return __uint_as_float(__reduce_max_sync(kFull, m));
 }
 
-// Dense large fill (many empty pixels in a warp's 2-row pair): one pass for
-// the vertical 31-row maxima of both rows c0, c0+1 over the warp's columns
-// L-11 .. L+140 into V[2][kVC] (rows [c0-14, c0+15] are shared), then each lane
-// takes the horizontal 31-max of its own empty pixels from V.
+// Dense large fill (many empty pixels in a warp's block): one pass for the
+// vertical 31-row maxima of the block's four rows over the warp's columns
+// L-11 .. L+140 into V[4][kVC] (34 ring rows per column), then each lane takes
+// the horizontal 31-max of its own empty pixels from V.
 constexpr int kVC = 152, kVOff = 11, kDenseMin = 12;
 
 template <int PLAG>
-__device__ __noinline__ void lf_vpair(const float* __restrict__ ring, int ringw, int p0, int p1, int H, int L,
+__device__ __noinline__ void lf_vquad(const float* __restrict__ ring, int ringw, int p0, int p1, int H, int L,
                                       int lane, int c0, bool consecutive, float* __restrict__ V) {
+  // vertical 31-maxima of rows c0 .. c0+3 (windows [c_j - 15, c_j + 15]); the
+  // rows [c0-12, c0+15] are common to all four
 #pragma unroll 1
   for (int sc = lane; sc < kVC; sc += 32) {
     const int col = L - kVOff + sc;
-    float o0 = 0.f, o1 = 0.f;
+    float o[kB] = {0.f, 0.f, 0.f, 0.f};
     if (col >= p0 && col < p1) {
       const float* rc = ring + (col - p0);
       auto ld = [&](int r) {
@@ -432,23 +434,27 @@ __device__ __noinline__ void lf_vpair(const float* __restrict__ ring, int ringw,
         return rc[((rr + PLAG) % kRing) * ringw];
       };
       if (consecutive) {
-        float core = ld(c0 - 14);
-#pragma unroll 10
-        for (int r = c0 - 13; r <= c0 + 15; ++r) core = fmx(core, ld(r));
-        o0 = fmx(core, ld(c0 - 15));
-        o1 = fmx(core, ld(c0 + 16));
+        float core = ld(c0 - 12);
+#pragma unroll 9
+        for (int r = c0 - 11; r <= c0 + 15; ++r) core = fmx(core, ld(r));
+        const float u15 = ld(c0 - 15), u14 = ld(c0 - 14), u13 = ld(c0 - 13);
+        const float d16 = ld(c0 + 16), d17 = ld(c0 + 17), d18 = ld(c0 + 18);
+        o[0] = fmx(core, fmx3(u15, u14, u13));
+        o[1] = fmx3(core, fmx(u14, u13), d16);
+        o[2] = fmx3(core, u13, fmx(d16, d17));
+        o[3] = fmx(core, fmx3(d16, d17, d18));
       } else {  // frame ends: each row centre clamped separately
-        const int ca = min(max(c0, 0), H - 1), cb = min(max(c0 + 1, 0), H - 1);
-        float m = ld(ca - kLF);
-        for (int r = ca - kLF + 1; r <= ca + kLF; ++r) m = fmx(m, ld(r));
-        o0 = m;
-        m = ld(cb - kLF);
-        for (int r = cb - kLF + 1; r <= cb + kLF; ++r) m = fmx(m, ld(r));
-        o1 = m;
+#pragma unroll
+        for (int j = 0; j < kB; ++j) {
+          const int cj = min(max(c0 + j, 0), H - 1);
+          float m = ld(cj - kLF);
+          for (int r = cj - kLF + 1; r <= cj + kLF; ++r) m = fmx(m, ld(r));
+          o[j] = m;
+        }
       }
     }
-    V[sc] = o0;
-    V[kVC + sc] = o1;
+#pragma unroll
+    for (int j = 0; j < kB; ++j) V[j * kVC + sc] = o[j];
   }
   __syncwarp();
 }
@@ -754,23 +760,19 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
       if (S.hasL) mb_wait(S.mbL + (g & 3) * 8, (g >> 2) & 1);
       if (S.hasR) mb_wait(S.mbR + (g & 3) * 8, (g >> 2) & 1);
       if (DENSE && __reduce_add_sync(kFull, __popc(em)) > kDenseMin) {
-        float* V = S.ring + kRing * S.ringw + p.nw * (kB * 128) + (threadIdx.x >> 5) * (2 * kVC);
+        float* V = S.ring + kRing * S.ringw + p.nw * (kB * 128) + (threadIdx.x >> 5) * (kB * kVC);
+        lf_vquad<LG::P>(S.ring, S.ringw, S.p0, S.p1, H, S.L, S.lane, tc0, !EDGE || (tc0 >= 0 && tc0 + kB - 1 < H),
+                        V);
 #pragma unroll
-        for (int j2 = 0; j2 < kB; j2 += 2) {
-          if (!__any_sync(kFull, ((em >> (4 * j2)) & 0xFFu) != 0)) continue;
-          lf_vpair<LG::P>(S.ring, S.ringw, S.p0, S.p1, H, S.L, S.lane, tc0 + j2,
-                          !EDGE || (tc0 + j2 >= 0 && tc0 + j2 + 1 < H), V);
+        for (int j = 0; j < kB; ++j)
 #pragma unroll
-          for (int jj = 0; jj < 2; ++jj)
-#pragma unroll
-            for (int c = 0; c < 4; ++c)
-              if (em >> (4 * (j2 + jj) + c) & 1u) {
-                const float r = lf_hpixel(V, jj, S.lane, c);
-                v6[j2 + jj].v[c] = r;
-                S.still_empty |= !(r > kValid);
-              }
-          __syncwarp();
-        }
+          for (int c = 0; c < 4; ++c)
+            if (em >> (4 * j + c) & 1u) {
+              const float r = lf_hpixel(V, j, S.lane, c);
+              v6[j].v[c] = r;
+              S.still_empty |= !(r > kValid);
+            }
+        __syncwarp();
         lanes = 0;
       }
       while (lanes) {

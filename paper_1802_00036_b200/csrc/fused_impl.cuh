@@ -468,6 +468,18 @@ __device__ __forceinline__ float lf_hpixel(const float* __restrict__ V, int j, i
   return m;
 }
 
+// all four columns of the lane at once: windows [x_c - 15, x_c + 15] share
+// [x_0 - 12, x_0 + 15]
+__device__ __forceinline__ F4 lf_hquad(const float* __restrict__ V, int j, int lane) {
+  const float* vr = V + j * kVC + 4 * lane + kVOff;  // <-> column x_0 = L + 4 lane
+  float core = vr[-12];
+#pragma unroll 9
+  for (int d = -11; d <= 15; ++d) core = fmx(core, vr[d]);
+  const float u15 = vr[-15], u14 = vr[-14], u13 = vr[-13], d16 = vr[16], d17 = vr[17], d18 = vr[18];
+  return F4{{fmx(core, fmx3(u15, u14, u13)), fmx3(core, fmx(u14, u13), d16), fmx3(core, u13, fmx(d16, d17)),
+             fmx(core, fmx3(d16, d17, d18))}};
+}
+
 // ---------------------------------------------------------------------------
 // per-item state and one 4-row iteration (EDGE: rows may leave the frame)
 // ---------------------------------------------------------------------------
@@ -764,14 +776,26 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
         lf_vquad<LG::P>(S.ring, S.ringw, S.p0, S.p1, H, S.L, S.lane, tc0, !EDGE || (tc0 >= 0 && tc0 + kB - 1 < H),
                         V);
 #pragma unroll
-        for (int j = 0; j < kB; ++j)
+        for (int j = 0; j < kB; ++j) {
+          const unsigned rowm = (em >> (4 * j)) & 0xFu;
+          if (__popc(rowm) >= 2) {  // the lane's four windows together
+            const F4 h = lf_hquad(V, j, S.lane);
 #pragma unroll
-          for (int c = 0; c < 4; ++c)
-            if (em >> (4 * j + c) & 1u) {
-              const float r = lf_hpixel(V, j, S.lane, c);
-              v6[j].v[c] = r;
-              S.still_empty |= !(r > kValid);
-            }
+            for (int c = 0; c < 4; ++c)
+              if (rowm >> c & 1u) {
+                v6[j].v[c] = h.v[c];
+                S.still_empty |= !(h.v[c] > kValid);
+              }
+          } else if (rowm) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              if (rowm >> c & 1u) {
+                const float r = lf_hpixel(V, j, S.lane, c);
+                v6[j].v[c] = r;
+                S.still_empty |= !(r > kValid);
+              }
+          }
+        }
         __syncwarp();
         lanes = 0;
       }

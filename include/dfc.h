@@ -35,6 +35,7 @@
  *   dfc_encode_raw16          kitti_io.py:60-65 (rint(f64(d) * 256) clipped, < 256 m check)
  *   dfc_error_sums            metrics.py:119-137 (_error_sums, per frame; MetricsAccumulator sums them)
  *   dfc_error_map             metrics.py:101-108 (error_map)
+ *   dfc_colormap              kitti_io.py:69-85 (write_colormap_png pixel values; PNG encoding stays on the host)
  */
 #ifndef DFC_H_
 #define DFC_H_
@@ -201,6 +202,9 @@ int dfc_error_sums(const float* pred, const float* gt, int64_t B, int32_t H, int
                    void* stream);
 /* out = |f64(pred) - f64(gt)| (float32) where both are valid, else 0 */
 int dfc_error_map(const float* pred, const float* gt, float* out, int64_t B, int32_t H, int32_t W, void* stream);
+/* rgb[n][3] (uint8) = the blue -> cyan -> green -> yellow -> red ramp of clip((v - lo) / (hi - lo), 0, 1),
+ * black where v == 0; DFC_E_INVALID unless hi > lo */
+int dfc_colormap(const float* values, uint8_t* rgb, int64_t n, double range_min, double range_max, void* stream);
 
 #ifdef __cplusplus
 }

@@ -55,3 +55,20 @@ def encode_raw16(values: np.ndarray) -> np.ndarray:
         raise ValueError("depth values must be < 256 m to be encodable")
     raw = np.rint(values.astype(np.float64) * DEPTH_SCALE)
     return np.clip(raw, 0, 65535).astype(np.uint16)
+
+
+_RAMP_X = np.array([0.0, 0.25, 0.5, 0.75, 1.0])           # kitti_io.py:27
+_RAMP = (np.array([0.0, 0.0, 0.0, 255.0, 255.0]),        # red    kitti_io.py:28
+         np.array([0.0, 255.0, 255.0, 255.0, 0.0]),      # green  kitti_io.py:29
+         np.array([255.0, 255.0, 0.0, 0.0, 0.0]))        # blue   kitti_io.py:30
+
+
+def colormap(values: np.ndarray, range_min: float, range_max: float) -> np.ndarray:
+    """kitti_io.write_colormap_png's pixel array (kitti_io.py:69-85), before PNG encoding."""
+    if range_max <= range_min:
+        raise ValueError(f"degenerate range [{range_min}, {range_max}]")
+    t = np.clip((values.astype(np.float64) - range_min) / (range_max - range_min), 0.0, 1.0)
+    rgb = np.stack([np.rint(np.interp(t, _RAMP_X, ch)) for ch in _RAMP], axis=-1).astype(np.uint8)
+    rgb[values == 0.0] = 0
+    return rgb
+

@@ -43,7 +43,7 @@ EXPORTS = (
     "dfc_offsets_max", "dfc_offsets_min", "dfc_median", "dfc_gaussian_separable", "dfc_bilateral",
     "dfc_invert", "dfc_validate", "dfc_masked_fill", "dfc_extend_to_top", "dfc_count_empty",
     "dfc_reimpose", "dfc_workspace_bytes_raw16", "dfc_fill_batch_raw16", "dfc_decode_raw16", "dfc_encode_raw16",
-    "dfc_error_sums", "dfc_error_map",
+    "dfc_error_sums", "dfc_error_map", "dfc_colormap",
 )
 
 
@@ -135,6 +135,7 @@ def load(require: bool = True):
         "dfc_encode_raw16": (ctypes.c_int, [vp, vp, i64, i64, vp, vp]),
         "dfc_error_sums": (ctypes.c_int, [vp, vp, i64, i32, i32, vp, vp, vp]),
         "dfc_error_map": (ctypes.c_int, [vp, vp, vp, i64, i32, i32, vp]),
+        "dfc_colormap": (ctypes.c_int, [vp, vp, i64, ctypes.c_double, ctypes.c_double, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

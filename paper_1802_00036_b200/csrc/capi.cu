@@ -639,4 +639,14 @@ int dfc_error_map(const float* pred, const float* gt, float* out, int64_t B, int
   return DFC_OK;
 }
 
+int dfc_colormap(const float* values, uint8_t* rgb, int64_t n, double range_min, double range_max, void* stream) {
+  if (!(range_max > range_min))
+    return fail(DFC_E_INVALID, "degenerate range [" + std::to_string(range_min) + ", " + std::to_string(range_max) + "]");
+  if (n < 0) return fail(DFC_E_INVALID, "negative size");
+  if (n == 0) return DFC_OK;
+  if (!values || !rgb) return fail(DFC_E_INVALID, "null buffer");
+  DFC_CK(dfc::launch_colormap(values, rgb, n, range_min, range_max, as_stream(stream)));
+  return DFC_OK;
+}
+
 }  // extern "C"

@@ -82,6 +82,7 @@ cudaError_t launch_encode_raw16(const float* in, uint16_t* out, int64_t n_per_fr
                                 cudaStream_t s);
 cudaError_t launch_error_sums(const float* pred, const float* gt, int64_t B, int64_t HW, double* sums,
                               int64_t* counts, cudaStream_t s);
+cudaError_t launch_colormap(const float* values, uint8_t* rgb, int64_t n, double lo, double hi, cudaStream_t s);
 cudaError_t launch_error_map(const float* pred, const float* gt, float* out, int64_t n, cudaStream_t s);
 cudaError_t launch_reimpose(const float* blurred, const float* mask_src, float* out, int64_t n, cudaStream_t s);
 cudaError_t launch_bin_select(const float* direct, const float* inv, float* out, int64_t n, float lo, float hi,

@@ -7,6 +7,8 @@
 // error_map (metrics.py:101-108): |f64(d) - f64(g)| rounded to float32 where
 // both are valid, 0 elsewhere.
 //
+// colormap: the visualisation of kitti_io.write_colormap_png.
+//
 // One CTA per frame, fixed reduction order (per-thread strided sums, warp
 // butterfly, then the warps in order), so a frame's sums are reproducible run
 // to run.  The reference's np.dot / np.sum order is unspecified (BLAS /
@@ -91,7 +93,57 @@ __global__ void error_map_kernel(const float* __restrict__ pred, const float* __
   }
 }
 
+// kitti_io.write_colormap_png's pixel arithmetic (kitti_io.py:69-85): t =
+// clip((f64(v) - lo) / (hi - lo), 0, 1); per channel numpy.interp on the
+// 5-stop ramp, i.e. slope_j * (t - x_j) + y_j for x_j <= t < x_{j+1} (y_4 at
+// t == 1), each operation rounded separately; rint to uint8; black where
+// v == 0.  float64 without contraction: bit-identical to numpy.
+struct Ramp {
+  double lo, span;
+  double x[5];
+  double y[3][5];
+  double slope[3][4];
+};
+
+__global__ void colormap_kernel(const float* __restrict__ v, uint8_t* __restrict__ rgb, int64_t n,
+                                const __grid_constant__ Ramp r) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float val = v[i];
+    double t = __ddiv_rn(__dsub_rn((double)val, r.lo), r.span);
+    t = fmin(fmax(t, 0.0), 1.0);
+    const int j = t >= r.x[3] ? 3 : (t >= r.x[2] ? 2 : (t >= r.x[1] ? 1 : 0));
+    uint8_t o[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double y = t >= r.x[4] ? r.y[c][4] : __dadd_rn(__dmul_rn(r.slope[c][j], __dsub_rn(t, r.x[j])), r.y[c][j]);
+      o[c] = val == 0.0f ? (uint8_t)0 : (uint8_t)rint(y);
+    }
+    rgb[3 * i] = o[0];
+    rgb[3 * i + 1] = o[1];
+    rgb[3 * i + 2] = o[2];
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_colormap(const float* values, uint8_t* rgb, int64_t n, double lo, double hi, cudaStream_t s) {
+  Ramp r;
+  r.lo = lo;
+  r.span = hi - lo;
+  const double x[5] = {0.0, 0.25, 0.5, 0.75, 1.0};
+  const double y[3][5] = {{0.0, 0.0, 0.0, 255.0, 255.0}, {0.0, 255.0, 255.0, 255.0, 0.0},
+                          {255.0, 255.0, 0.0, 0.0, 0.0}};  // kitti_io.py:27-31 ramp stops
+  for (int k = 0; k < 5; ++k) r.x[k] = x[k];
+  for (int c = 0; c < 3; ++c)
+    for (int k = 0; k < 5; ++k) {
+      r.y[c][k] = y[c][k];
+      if (k < 4) r.slope[c][k] = (y[c][k + 1] - y[c][k]) / (x[k + 1] - x[k]);
+    }
+  const int64_t blocks = (n + 255) / 256;
+  note_launch();
+  colormap_kernel<<<(unsigned)(blocks < 148 * 32 ? blocks : 148 * 32), 256, 0, s>>>(values, rgb, n, r);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_error_sums(const float* pred, const float* gt, int64_t B, int64_t HW, double* sums,
                               int64_t* counts, cudaStream_t s) {

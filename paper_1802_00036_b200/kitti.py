@@ -57,3 +57,19 @@ def complete_raw16_batch(raw, config: PipelineConfig | None = None, out_raw: boo
     if raise_on_error:
         raise_for_status(res.status.cpu().numpy(), _max_depth(config))
     return res
+
+
+def colormap(values, range_min: float, range_max: float) -> torch.Tensor:
+    """write_colormap_png's pixels (kitti_io.py:69-85) on the GPU: uint8 [..., 3] on the
+    blue -> red ramp of clip((v - lo) / (hi - lo), 0, 1), black where v == 0."""
+    if range_max <= range_min:
+        raise ValueError(f"degenerate range [{range_min}, {range_max}]")
+    v = values if isinstance(values, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(values, np.float32))
+    if v.device.type != "cuda":
+        v = v.to(_device())
+    v = v.contiguous()
+    rgb = torch.empty(tuple(v.shape) + (3,), dtype=torch.uint8, device=v.device)
+    _lib.check(_lib.load().dfc_colormap(ops._ptr(v), ops._ptr(rgb), v.numel(), float(range_min), float(range_max),
+                                        ops._stream()))
+    return rgb
+

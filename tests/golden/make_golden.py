@@ -350,6 +350,18 @@ def gen_kitti():
 
         Image.fromarray(raw).save(path)
         out["all_raw_decoded"] = np.array(kitti_io.read_depth_png(path).values)
+        # colormap rendering (kitti_io.write_colormap_png): pixels read back from the PNG
+        ranges = [(0.0, 80.0), (2.5, 7.25), (-1.0, 0.5)]
+        for k, (lo, hi) in enumerate(ranges):
+            v = rng.uniform(lo - 5.0, hi + 5.0, size=(33, 47)).astype(np.float32)
+            v[rng.random(v.shape) < 0.2] = 0.0
+            v.flat[1:6] = np.float32(lo + (hi - lo) * np.array([0.0, 0.25, 0.5, 0.75, 1.0]))  # ramp stops
+            path = tmp / f"c{k}.png"
+            kitti_io.write_colormap_png(v, path, lo, hi)
+            with Image.open(path) as img:
+                out[f"cmap_rgb_{k}"] = np.array(img.convert("RGB"))
+            out[f"cmap_in_{k}"] = v
+            out[f"cmap_range_{k}"] = np.array([lo, hi])
     finally:
         shutil.rmtree(tmp, ignore_errors=True)
     np.savez_compressed(HERE / "kitti_small.npz", **out)

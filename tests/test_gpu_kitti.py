@@ -114,3 +114,19 @@ def test_raw16_errors(K):
     empty = np.full((1, 64, 128), 25, np.uint16)  # 25 / 256 <= 0.1 m: every pixel empty
     with pytest.raises(P.DegenerateInputError):
         K.complete_raw16_batch(empty, P.PipelineConfig())
+
+
+def test_colormap_vs_oracle(K, golden_dir):
+    """GPU colormap pixels bit-identical to the oracle (pinned to write_colormap_png) and to the golden PNGs."""
+    from oracle import metrics_oracle as M
+
+    z = np.load(golden_dir / "kitti_small.npz")
+    for k in range(3):
+        lo, hi = (float(x) for x in z[f"cmap_range_{k}"])
+        assert np.array_equal(K.colormap(z[f"cmap_in_{k}"], lo, hi).cpu().numpy(), z[f"cmap_rgb_{k}"])
+    rng = np.random.default_rng(8)
+    v = rng.uniform(-10, 120, size=(2, 200, 300)).astype(np.float32)
+    v[rng.random(v.shape) < 0.3] = 0.0
+    assert np.array_equal(K.colormap(v, 0.0, 100.0).cpu().numpy(), M.colormap(v, 0.0, 100.0))
+    with pytest.raises(ValueError, match="degenerate range"):
+        K.colormap(v, 5.0, 5.0)

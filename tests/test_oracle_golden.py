@@ -157,3 +157,13 @@ def test_kitti_oracle_matches_reference_png_roundtrip(golden_dir):
         assert np.array_equal(back.view(np.uint32), z[f"back_{k}"].view(np.uint32))
     raw = np.arange(65536, dtype=np.uint16).reshape(256, 256)
     assert np.array_equal(M.decode_raw16(raw).view(np.uint32), z["all_raw_decoded"].view(np.uint32))
+
+
+def test_colormap_oracle_matches_reference_png(golden_dir):
+    """oracle colormap against kitti_io.write_colormap_png's PNG pixels."""
+    from oracle import metrics_oracle as M
+
+    z = np.load(golden_dir / "kitti_small.npz")
+    for k in range(3):
+        lo, hi = z[f"cmap_range_{k}"]
+        assert np.array_equal(M.colormap(z[f"cmap_in_{k}"], float(lo), float(hi)), z[f"cmap_rgb_{k}"])

@@ -182,8 +182,10 @@ int dfc_reimpose(const float* blurred, const float* mask_src, float* out, int64_
  * raw_in: [B][H][W] uint16, depth = raw / 256 m, raw 0 = empty.
  * out: float32 depth (out_raw == 0) or uint16 raw (out_raw != 0, rint(depth * 256)
  * clipped to [0, 65535]; frames with an output >= 256 m get DFC_ST_ENCODE).
- * Same config, status and iteration semantics as dfc_fill_batch; the fallback
- * frames are finished inside the call (DFC_F_NO_FINISH is ignored). */
+ * Same config, status and iteration semantics as dfc_fill_batch.  Frames that
+ * need more than one large-fill iteration are finished inside the call unless
+ * DFC_F_NO_FINISH is set: then (fused path only) they keep status bit 0x200 and
+ * the caller re-runs them, e.g. with DFC_F_FORCE_STAGED. */
 size_t dfc_workspace_bytes_raw16(const dfc_config* cfg, int64_t B, int32_t H, int32_t W);
 int dfc_fill_batch_raw16(const uint16_t* raw_in, void* out, int32_t out_raw, int64_t B, int32_t H, int32_t W,
                          const dfc_config* cfg, uint32_t* frame_status, int32_t* large_fill_iters, void* workspace,

@@ -565,6 +565,7 @@ int dfc_fill_batch_raw16(const uint16_t* raw_in, void* out, int32_t out_raw, int
     if (large_fill_iters) DFC_CK(cudaMemsetAsync(large_fill_iters, 0, B * 4, s));
     DFC_CK(dfc::launch_fused(raw_in, out, B, H, W, c, frame_status, large_fill_iters, ws, L.fused, s,
                              out_raw ? 2 : 1));
+    if (c.flags & DFC_F_NO_FINISH) return DFC_OK;  // the caller re-runs frames with status bit 0x200
     unsigned long long nfb = 0;
     DFC_CK(cudaMemcpyAsync(&nfb, ws, 8, cudaMemcpyDeviceToHost, s));
     DFC_CK(cudaStreamSynchronize(s));

@@ -73,3 +73,62 @@ def colormap(values, range_min: float, range_max: float) -> torch.Tensor:
                                         ops._stream()))
     return rgb
 
+
+class RawPipeline:
+    """KITTI raw frames in pinned host memory -> GPU -> raw frames in pinned host
+    memory, like completion.HostPipeline: chunk k's copies and launch go to stream
+    k % n_streams so both copy directions overlap computation; 2 B/px each way.
+    Frames the fused kernel flags for more large-fill iterations are re-run
+    through the staged path at the end."""
+
+    def __init__(self, config: PipelineConfig | None = None, chunk: int = 64, n_streams: int = 3, device=None):
+        self.config = config or PipelineConfig()
+        self.chunk = int(chunk)
+        self.device = torch.device(device) if device is not None else _device()
+        self.streams = [torch.cuda.Stream(self.device) for _ in range(n_streams)]
+        self.cfg = to_dfc_config(self.config)
+        self.cfg.flags |= _lib.F_NO_FINISH
+        self._bufs = None
+
+    def _alloc(self, H, W):
+        if self._bufs is None or self._bufs[0] != (H, W):
+            self._bufs = ((H, W), [(torch.empty((self.chunk, H, W), dtype=torch.uint16, device=self.device),
+                                    torch.empty((self.chunk, H, W), dtype=torch.uint16, device=self.device),
+                                    ops.Workspace()) for _ in self.streams])
+        return self._bufs[1]
+
+    def run(self, host_in: torch.Tensor, host_out: torch.Tensor | None = None, raise_on_error: bool = True):
+        """host_in: [B, H, W] uint16 CPU tensor (pinned for full overlap); returns (host_out, status, iterations)."""
+        B, H, W = host_in.shape
+        if host_out is None:
+            host_out = torch.empty((B, H, W), dtype=torch.uint16, pin_memory=True)
+        bufs = self._alloc(H, W)
+        status = torch.empty(B, dtype=torch.int32, device=self.device)
+        iters = torch.empty(B, dtype=torch.int32, device=self.device)
+        cur = torch.cuda.current_stream(self.device)
+        for s in self.streams:
+            s.wait_stream(cur)
+        for k, a in enumerate(range(0, B, self.chunk)):
+            b = min(B, a + self.chunk)
+            s = self.streams[k % len(self.streams)]
+            d_in, d_out, ws = bufs[k % len(self.streams)]
+            with torch.cuda.stream(s):
+                d_in[: b - a].copy_(host_in[a:b], non_blocking=True)
+                ops.fill_batch_raw16(d_in[: b - a], self.cfg, out_raw=True, workspace=ws, out=d_out[: b - a],
+                                     status=status[a:b], iterations=iters[a:b])
+                host_out[a:b].copy_(d_out[: b - a], non_blocking=True)
+        for s in self.streams:
+            cur.wait_stream(s)
+        st = status.cpu()
+        it = iters.cpu()
+        need = torch.nonzero(st & 0x200).flatten().tolist()
+        if need:  # rare: frames needing more than one large-fill iteration
+            raw_need = host_in.view(torch.int16)[need].view(torch.uint16)  # (no uint16 gather / scatter in torch)
+            res = complete_raw16_batch(raw_need, self.config, out_raw=True, raise_on_error=False, force_staged=True)
+            host_out.view(torch.int16)[need] = res.dense.cpu().view(torch.int16)
+            st[need] = res.status.cpu() | _lib.ST_FALLBACK
+            it[need] = res.iterations.cpu()
+        if raise_on_error:
+            raise_for_status(st.numpy(), _max_depth(self.config))
+        return host_out, st, it
+

@@ -229,7 +229,8 @@ def fill_batch(frames: torch.Tensor, cfg: "_lib.DfcConfig", out: torch.Tensor | 
 # ---------------------------------------------------------------------------
 
 def fill_batch_raw16(raw: torch.Tensor, cfg: "_lib.DfcConfig", out_raw: bool = True,
-                     workspace: Workspace | None = None) -> FillResult:
+                     workspace: Workspace | None = None, out: torch.Tensor | None = None,
+                     status: torch.Tensor | None = None, iterations: torch.Tensor | None = None) -> FillResult:
     """dfc_fill_batch_raw16: uint16 raw frames in; uint16 raw (or float32 depth) out."""
     if raw.dtype != torch.uint16:
         raise TypeError("raw frames must be torch.uint16")
@@ -245,9 +246,12 @@ def fill_batch_raw16(raw: torch.Tensor, cfg: "_lib.DfcConfig", out_raw: bool = T
     if workspace is None:
         workspace = _default_ws.setdefault(x.device, Workspace())
     ws = workspace.get(need, x.device)
-    out = torch.empty(x.shape, dtype=torch.uint16 if out_raw else torch.float32, device=x.device)
-    status = torch.empty(B, dtype=torch.int32, device=x.device)
-    iterations = torch.empty(B, dtype=torch.int32, device=x.device)
+    if out is None:
+        out = torch.empty(x.shape, dtype=torch.uint16 if out_raw else torch.float32, device=x.device)
+    if status is None:
+        status = torch.empty(B, dtype=torch.int32, device=x.device)
+    if iterations is None:
+        iterations = torch.empty(B, dtype=torch.int32, device=x.device)
     check(L.dfc_fill_batch_raw16(_ptr(x), _ptr(out), int(out_raw), B, H, W, ctypes.byref(cfg), _ptr(status),
                                  _ptr(iterations), _ptr(ws), ws.numel(), _stream()))
     return FillResult(out, status, iterations)

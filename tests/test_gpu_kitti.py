@@ -130,3 +130,22 @@ def test_colormap_vs_oracle(K, golden_dir):
     assert np.array_equal(K.colormap(v, 0.0, 100.0).cpu().numpy(), M.colormap(v, 0.0, 100.0))
     with pytest.raises(ValueError, match="degenerate range"):
         K.colormap(v, 5.0, 5.0)
+
+
+def test_raw_pipeline_matches_batch_api(K):
+    """Pinned-host raw16 pipeline (3 streams, chunks) == complete_raw16_batch, incl. a frame that
+    needs more than one large-fill iteration (re-run through the staged path)."""
+    import paper_1802_00036_b200 as P
+
+    raw = _raw_frames(1, 10, 61)
+    rng = np.random.default_rng(4)
+    f = np.zeros_like(raw[3])
+    f.flat[rng.choice(f.size, 4, replace=False)] = rng.integers(600, 20000, 4).astype(np.uint16)
+    raw[3] = f  # 4 isolated points: several large-fill iterations
+    cfg = P.PipelineConfig(blur_mode=P.BlurMode.GAUSSIAN, fill_mode=P.FillMode.FULL)
+    want = K.complete_raw16_batch(raw, cfg)
+    pipe = K.RawPipeline(cfg, chunk=4)
+    out, st, it = pipe.run(torch.from_numpy(raw).pin_memory())
+    assert np.array_equal(out.numpy(), want.dense.cpu().numpy())
+    assert np.array_equal(it.numpy(), want.iterations.cpu().numpy())
+    assert int(it[3]) > 1 and int(st[3]) & 0x100  # finished by the staged path

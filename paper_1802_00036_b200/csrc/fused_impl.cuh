@@ -277,7 +277,7 @@ __device__ __forceinline__ void load_bits(const T* frame, int H, int W, int x0, 
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const int y = y0 + 16 * h + i;
-      if (y < H)
+      if (y >= 0 && y < H)
         v[i] = load4_t<VEC>(frame + (int64_t)y * W, x0, W);
       else
         set_row(v[i], 0.f);
@@ -330,18 +330,20 @@ __device__ __forceinline__ void hcomb(const uint64_t in[4], uint64_t out[4]) {
 
 template <int VEC, bool PRE, typename T>
 __device__ __forceinline__ void phase1(const T* frame, const Params& p, int x0, bool needed, unsigned incol,
-                                       int T0[4], unsigned& umax) {
+                                       int T0[4], unsigned& umax, int s0 = 0) {
+  // blocks start at row s0; rows above s0 hold no (inverted-)valid pixel
   const int H = p.H, W = p.W;
   uint32_t prv[4] = {0, 0, 0, 0}, cur[4], nxt[4];
-  load_bits<VEC, PRE>(frame, H, W, x0, 0, p.md, cur, umax);
-  load_bits<VEC, PRE>(frame, H, W, x0, 32, p.md, nxt, umax);  // (T deduced)
+  load_bits<VEC, PRE>(frame, H, W, x0, s0, p.md, cur, umax);
+  load_bits<VEC, PRE>(frame, H, W, x0, s0 + 32, p.md, nxt, umax);  // (T deduced)
   int r0[4] = {-1, -1, -1, -1};
   uint64_t cm[4];
 #pragma unroll
   for (int c = 0; c < 4; ++c) cm[c] = (incol >> c & 1) ? ~0ull : 0ull;
-  for (int b = 0; 32 * b < H; ++b) {
+  for (int b = 0; s0 + 32 * b < H; ++b) {
     uint64_t X[4], A[4], Bq[4];
-    const int lo = max(0, 16 - 32 * b), hi = min(64, H - 32 * b + 16);
+    const int ylo = s0 + 32 * b - 16;  // window bit i <-> row ylo + i
+    const int lo = max(0, -ylo), hi = min(64, H - ylo);
     const uint64_t inrow = (hi <= lo) ? 0ull : ((hi - lo == 64) ? ~0ull : (((1ull << (hi - lo)) - 1) << lo));
 #pragma unroll
     for (int c = 0; c < 4; ++c)
@@ -371,7 +373,7 @@ __device__ __forceinline__ void phase1(const T* frame, const Params& p, int x0, 
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const uint32_t cand = (uint32_t)((Bq[c] & inrow & cm[c]) >> 16);
-      if (r0[c] < 0 && cand) r0[c] = 32 * b + __ffs(cand) - 1;
+      if (r0[c] < 0 && cand) r0[c] = s0 + 32 * b + __ffs(cand) - 1;
       done = done && (r0[c] >= 0 || !(incol >> c & 1));
     }
     if (__all_sync(kFull, done || !needed)) break;
@@ -380,7 +382,7 @@ __device__ __forceinline__ void phase1(const T* frame, const Params& p, int x0, 
       prv[c] = cur[c];
       cur[c] = nxt[c];
     }
-    load_bits<VEC, PRE>(frame, H, W, x0, 32 * (b + 2), p.md, nxt, umax);
+    load_bits<VEC, PRE>(frame, H, W, x0, s0 + 32 * (b + 2), p.md, nxt, umax);
   }
 #pragma unroll
   for (int c = 0; c < 4; ++c) T0[c] = r0[c] >= 0 ? (H - 1 - r0[c]) : INT_MAX;
@@ -1071,6 +1073,36 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
 // records the largest input bit pattern of the rows it scanned (the top rows,
 // which phase 2 does not read).  One 32-row block costs a global-load round
 // trip; many warps per SM hide it, which the fused kernel's 12 could not.
+// First row (from the top, a multiple of 16) of the 16-row group holding the
+// warp's first valid pixel (H when none); tracks umax over the rows it reads.
+// Stage-4 validity reaches at most 7 rows above it (D_diamond 2 + D5 2 + D7 3),
+// so the exact scan can start 8 rows higher with all-empty rows before.
+template <int VEC, bool PRE, typename T>
+__device__ __forceinline__ int first_valid_group(const T* frame, int H, int W, int x0, unsigned& umax) {
+  int y = 0;
+  for (; y < H; y += 16) {
+    F4 v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      if (y + i < H)
+        v[i] = load4_t<VEC>(frame + (int64_t)(y + i) * W, x0, W);
+      else
+        set_row(v[i], 0.f);
+    }
+    float mx = 0.f;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      if constexpr (!PRE) {
+        umax = max(max(umax, __float_as_uint(v[i].v[0])), __float_as_uint(v[i].v[1]));
+        umax = max(max(umax, __float_as_uint(v[i].v[2])), __float_as_uint(v[i].v[3]));
+      }
+      mx = fmx3(mx, fmx3(v[i].v[0], v[i].v[1], v[i].v[2]), v[i].v[3]);
+    }
+    if (__any_sync(kFull, mx > kValid)) break;
+  }
+  return y;
+}
+
 template <int VEC, bool PRE, int IO>
 __global__ void __launch_bounds__(128, 4) r0_kernel(const __grid_constant__ Params p) {
   using TIn = typename IoT<IO>::In;
@@ -1092,7 +1124,8 @@ __global__ void __launch_bounds__(128, 4) r0_kernel(const __grid_constant__ Para
   const TIn* src = static_cast<const TIn*>(p.in) + frame * (int64_t)p.H * p.W;
   int T0[4];
   unsigned umax = 0;
-  phase1<VEC, PRE>(src, p, x0, own != 0, incol, T0, umax);
+  const int s0 = first_valid_group<VEC, PRE>(src, p.H, p.W, x0, umax) - 8;
+  phase1<VEC, PRE>(src, p, x0, own != 0, incol, T0, umax, s0);
   int32_t* dst = p.t0g + frame * p.W + x0;
 #pragma unroll
   for (int c = 0; c < 4; ++c)

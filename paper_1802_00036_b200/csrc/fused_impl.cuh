@@ -183,23 +183,6 @@ __device__ __forceinline__ F4 lds4_t(uint32_t saddr) {
   }
 }
 
-// one lane's 4 columns of a row, bounds-checked (phase 1)
-template <int VEC, typename T>
-__device__ __forceinline__ F4 load4_t(const T* row, int x0, int W) {
-  if constexpr (sizeof(T) == 4) {
-    return load4<VEC, false>(row, x0, W);
-  } else {
-    if (x0 >= 0 && x0 + 3 < W) {
-      const uint2 u = __ldg(reinterpret_cast<const uint2*>(row + x0));
-      return unpack_raw(u.x, u.y);
-    }
-    F4 r;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) r.v[c] = (x0 + c >= 0 && x0 + c < W) ? raw_m(__ldg(row + x0 + c)) : 0.0f;
-    return r;
-  }
-}
-
 // rint(depth * 256) clipped to [0, 65535] (kitti_io.py:62-65); depth * 256 is
 // exact, so round-to-nearest-even here equals numpy's float64 rint
 __device__ __forceinline__ unsigned enc_raw(float v) {
@@ -263,37 +246,100 @@ __device__ void item_geometry(int s, const Params& p, int warp, Geo& g) {
 // ---------------------------------------------------------------------------
 // Phase 1: first valid stage-4 row per column, bit-packed morphology
 // ---------------------------------------------------------------------------
-// bit i of w[c]: (inverted) validity of row y0 + i; PRE: the frame is the
-// stage-2 map in the inverted encoding already
+// One lane's 4 columns of successive rows for the r0 scan, read from clamped
+// addresses so no row needs a bounds check: columns outside the frame read
+// in-frame pixels, which only feed the validation max (harmless) and are
+// masked out of the validity bits by the caller's column mask.
+template <int VEC, typename T>
+struct LaneCols {
+  const T* a;  // VEC 4: the lane's clamped first column; VEC 2: pair 0; VEC 1: column 0
+  int o1, o2, o3;  // VEC 2: o2 = pair 1; VEC 1: columns 1..3 (offsets from a)
+  __device__ __forceinline__ LaneCols(const T* frame, int x0, int W) {
+    if constexpr (VEC == 4) {
+      a = frame + min(max(x0, 0), W - 4);
+      o1 = o2 = o3 = 0;
+    } else if constexpr (VEC == 2) {
+      const int c0 = min(max(x0, 0), W - 2);
+      a = frame + c0;
+      o1 = o3 = 0;
+      o2 = min(max(x0 + 2, 0), W - 2) - c0;
+    } else {
+      const int c0 = min(max(x0, 0), W - 1);
+      a = frame + c0;
+      o1 = min(max(x0 + 1, 0), W - 1) - c0;
+      o2 = min(max(x0 + 2, 0), W - 1) - c0;
+      o3 = min(max(x0 + 3, 0), W - 1) - c0;
+    }
+  }
+  // row at element offset off (= y * W)
+  __device__ __forceinline__ F4 row(int64_t off) const {
+    const T* q = a + off;
+    if constexpr (sizeof(T) == 2) {
+      static_assert(VEC == 4, "16-bit input needs W % 4 == 0");
+      const uint2 u = __ldg(reinterpret_cast<const uint2*>(q));
+      return unpack_raw(u.x, u.y);
+    } else if constexpr (VEC == 4) {
+      const float4 t = __ldg(reinterpret_cast<const float4*>(q));
+      return F4{{t.x, t.y, t.z, t.w}};
+    } else if constexpr (VEC == 2) {
+      const float2 u = __ldg(reinterpret_cast<const float2*>(q));
+      const float2 w = __ldg(reinterpret_cast<const float2*>(q + o2));
+      return F4{{u.x, u.y, w.x, w.y}};
+    } else {
+      return F4{{__ldg(q), __ldg(q + o1), __ldg(q + o2), __ldg(q + o3)}};
+    }
+  }
+};
+
+// Inverted-encoding validity of one row's 4 columns as bits 0..3.  Frames
+// whose inputs are negative, non-finite or >= md are flagged by the
+// validation max and raise, so here 0 <= v < md and md - v > 0: the inverted
+// value md - v is valid iff min(v, md - v) > 0.1 (depth_core.py:150-156).
+template <bool PRE>
+__device__ __forceinline__ void row_bits(const F4& v, float md, int i, uint32_t w[4], unsigned& umax) {
+  if constexpr (PRE) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (v.v[c] > kValid) w[c] |= 1u << i;
+  } else {
+    umax = max(max(umax, __float_as_uint(v.v[0])), __float_as_uint(v.v[1]));
+    umax = max(max(umax, __float_as_uint(v.v[2])), __float_as_uint(v.v[3]));
+    const float2 d01 = __ffma2_rn(make_float2(v.v[0], v.v[1]), make_float2(-1.f, -1.f), make_float2(md, md));
+    const float2 d23 = __ffma2_rn(make_float2(v.v[2], v.v[3]), make_float2(-1.f, -1.f), make_float2(md, md));
+    const float d[4] = {d01.x, d01.y, d23.x, d23.y};
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (fminf(v.v[c], d[c]) > kValid) w[c] |= 1u << i;
+  }
+}
+
+// bit i of w[c]: (inverted) validity of row y0 + i (0 outside the frame);
+// PRE: the frame is the stage-2 map in the inverted encoding already
 template <int VEC, bool PRE, typename T>
-__device__ __forceinline__ void load_bits(const T* frame, int H, int W, int x0, int y0, float md, uint32_t w[4],
+__device__ __forceinline__ void load_bits(const LaneCols<VEC, T>& lc, int H, int W, int y0, float md, uint32_t w[4],
                                           unsigned& umax) {
 #pragma unroll
   for (int c = 0; c < 4; ++c) w[c] = 0;
   if (y0 >= H) return;
+  if (y0 >= 0 && y0 + 32 <= H) {
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    F4 v[16];
+    for (int h = 0; h < 2; ++h) {
+      F4 v[16];
+      const int64_t off = (int64_t)(y0 + 16 * h) * W;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int y = y0 + 16 * h + i;
-      if (y >= 0 && y < H)
-        v[i] = load4_t<VEC>(frame + (int64_t)y * W, x0, W);
-      else
-        set_row(v[i], 0.f);
+      for (int i = 0; i < 16; ++i) v[i] = lc.row(off + (int64_t)i * W);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) row_bits<PRE>(v[i], md, 16 * h + i, w, umax);
+    }
+  } else {
+    const uint32_t rows = (uint32_t)(((1ull << (min(H - y0, 32))) - 1) & ~((1ull << min(max(-y0, 0), 32)) - 1));
+#pragma unroll 4
+    for (int i = 0; i < 32; ++i) {
+      const int y = min(max(y0 + i, 0), H - 1);
+      row_bits<PRE>(lc.row((int64_t)y * W), md, i, w, umax);
     }
 #pragma unroll
-    for (int i = 0; i < 16; ++i)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        if constexpr (PRE) {
-          w[c] |= (uint32_t)(v[i].v[c] > kValid) << (16 * h + i);
-        } else {
-          umax = max(umax, __float_as_uint(v[i].v[c]));
-          const float inv = v[i].v[c] > kValid ? md - v[i].v[c] : 0.0f;
-          w[c] |= (uint32_t)(inv > kValid) << (16 * h + i);
-        }
-      }
+    for (int c = 0; c < 4; ++c) w[c] &= rows;
   }
 }
 
@@ -334,8 +380,9 @@ __device__ __forceinline__ void phase1(const T* frame, const Params& p, int x0, 
   // blocks start at row s0; rows above s0 hold no (inverted-)valid pixel
   const int H = p.H, W = p.W;
   uint32_t prv[4] = {0, 0, 0, 0}, cur[4], nxt[4];
-  load_bits<VEC, PRE>(frame, H, W, x0, s0, p.md, cur, umax);
-  load_bits<VEC, PRE>(frame, H, W, x0, s0 + 32, p.md, nxt, umax);  // (T deduced)
+  const LaneCols<VEC, T> lc(frame, x0, W);
+  load_bits<VEC, PRE>(lc, H, W, s0, p.md, cur, umax);
+  load_bits<VEC, PRE>(lc, H, W, s0 + 32, p.md, nxt, umax);
   int r0[4] = {-1, -1, -1, -1};
   uint64_t cm[4];
 #pragma unroll
@@ -382,7 +429,7 @@ __device__ __forceinline__ void phase1(const T* frame, const Params& p, int x0, 
       prv[c] = cur[c];
       cur[c] = nxt[c];
     }
-    load_bits<VEC, PRE>(frame, H, W, x0, s0 + 32 * (b + 2), p.md, nxt, umax);
+    load_bits<VEC, PRE>(lc, H, W, s0 + 32 * (b + 2), p.md, nxt, umax);
   }
 #pragma unroll
   for (int c = 0; c < 4; ++c) T0[c] = r0[c] >= 0 ? (H - 1 - r0[c]) : INT_MAX;
@@ -498,6 +545,14 @@ __device__ __forceinline__ void mb_arrive(uint32_t a) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(a) : "memory");
 }
 __device__ __forceinline__ void mb_wait(uint32_t a, uint32_t parity) {
+#ifdef DFC_EXP_SUSPEND
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1, %2;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(a),
+      "r"(parity), "r"(DFC_EXP_SUSPEND)
+      : "memory");
+  return;
+#endif
   asm volatile(
       "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
       " @!p bra WAIT_%=;\n}\n" ::"r"(a),
@@ -697,7 +752,11 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
   S.lrow = static_cast<const TIn*>(S.lrow) - kB * W;
   // --- ring store: ring slot of row t is (t + P) mod 40, so this block is slots 4*(k mod 10) + j ---
   const int g = S.gk++;
+#ifndef DFC_EXP_NOWAIT
   if (g >= 2) {
+#else
+  if (false) {
+#endif
     const uint32_t o = 32 + ((g - 2) & 3) * 8, ph = ((g - 2) >> 2) & 1;
     if (S.hasL) mb_wait(S.mbL + o, ph);
     if (S.hasR) mb_wait(S.mbR + o, ph);
@@ -762,7 +821,11 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
     for (int j = 0; j < kB; ++j)
 #pragma unroll
       for (int c = 0; c < 4; ++c) mn = fminf(mn, fmaxf(v6[j].v[c], S.nb[c]));
+#ifdef DFC_EXP_NOLF
+    if (false) {
+#else
     if (__any_sync(kFull, !(mn > kValid))) {
+#endif
       unsigned em = 0;  // bit 4j+c: needed empty pixel
 #pragma unroll
       for (int j = 0; j < kB; ++j)
@@ -771,8 +834,10 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
       S.had_empty |= em != 0;
       unsigned lanes = __ballot_sync(kFull, em != 0);
       // neighbours' rows up to tc0 + 18
+#ifndef DFC_EXP_NOWAIT
       if (S.hasL) mb_wait(S.mbL + (g & 3) * 8, (g >> 2) & 1);
       if (S.hasR) mb_wait(S.mbR + (g & 3) * 8, (g >> 2) & 1);
+#endif
       if (DENSE && __reduce_add_sync(kFull, __popc(em)) > kDenseMin) {
         float* V = S.ring + kRing * S.ringw + p.nw * (kB * 128) + (threadIdx.x >> 5) * (kB * kVC);
         lf_vquad<LG::P>(S.ring, S.ringw, S.p0, S.p1, H, S.L, S.lane, tc0, !EDGE || (tc0 >= 0 && tc0 + kB - 1 < H),
@@ -1079,15 +1144,19 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
 // so the exact scan can start 8 rows higher with all-empty rows before.
 template <int VEC, bool PRE, typename T>
 __device__ __forceinline__ int first_valid_group(const T* frame, int H, int W, int x0, unsigned& umax) {
+  // clamped columns / rows may add in-frame pixels of the warp's strip to the
+  // test: the group found can only be earlier, which is safe for the scan start
+  const LaneCols<VEC, T> lc(frame, x0, W);
   int y = 0;
   for (; y < H; y += 16) {
     F4 v[16];
+    if (y + 16 <= H) {
+      const int64_t off = (int64_t)y * W;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      if (y + i < H)
-        v[i] = load4_t<VEC>(frame + (int64_t)(y + i) * W, x0, W);
-      else
-        set_row(v[i], 0.f);
+      for (int i = 0; i < 16; ++i) v[i] = lc.row(off + (int64_t)i * W);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = lc.row((int64_t)min(y + i, H - 1) * W);
     }
     float mx = 0.f;
 #pragma unroll

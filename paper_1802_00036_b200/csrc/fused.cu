@@ -95,7 +95,7 @@ Layout layout_for(int W, int strips) {
     const int p1 = o1 == W ? W : std::min(W, (o1 + 17 + 3) & ~3);
     pwmax = std::max(pwmax, p1 - p0);
   }
-  const int ringw = (pwmax + 3) & ~3;
+  const int ringw = ring_width(pwmax);
   L.smem = (size_t)kRing * ringw * 4 + (size_t)L.nw * kB * 512;
   // dense large-fill scratch when it fits next to the ring (wide strips; a
   // whole 1216-wide frame's ring leaves no room -- its empties are sparse)

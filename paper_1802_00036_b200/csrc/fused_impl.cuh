@@ -211,6 +211,10 @@ __device__ __forceinline__ void store_lane_t(T* q, const F4& a, unsigned colmask
 // ---------------------------------------------------------------------------
 // per-item warp geometry
 // ---------------------------------------------------------------------------
+// ring row stride: >= the production columns, an odd multiple of 4 floats
+// (conflict-free row-per-lane float4 loads in lf_rows)
+__host__ __device__ __forceinline__ int ring_width(int pw) { return ((pw + 3) & ~3) | 4; }
+
 struct Geo {
   int o0, o1;  // output columns of the strip
   int p0, p1;  // stage-5 production (ring) columns
@@ -461,6 +465,45 @@ __device__ __forceinline__ float lf_one(const float* __restrict__ ring, int ring
   return __uint_as_float(__reduce_max_sync(kFull, m));
 }
 
+// The same pixel with the rows across lanes: lane i takes ring row row-15+i
+// and the max over its 31 window columns (nine aligned float4 loads, the
+// partial chunks masked); redux.max combines the rows.  The ring row stride is
+// an odd multiple of 4 floats (ring_width), so the lanes' 16-byte loads of one
+// chunk hit distinct banks.  Needs the whole window inside the strip's ring
+// columns: x - 15 >= p0 and x + 15 < p1.
+template <int PLAG>
+__device__ __forceinline__ float lf_rows(const float* __restrict__ ring, int ringw, int p0, int H, int lane, int x,
+                                         int row) {
+  const int t = row - kLF + lane;
+  unsigned m = 0u;
+  if (lane < 2 * kLF + 1 && t >= 0 && t < H) {
+    const int c0 = x - kLF - p0;  // first window column (ring index)
+    const int a = c0 & ~3, o = c0 - a;
+    const float* rp = ring + ((t + PLAG) % kRing) * ringw + a;
+    // the window is columns a+o .. a+o+30: chunk 0 (a .. a+3) counts from o,
+    // column a+31 needs o >= 1, a+32 / a+33 need o >= 2 / 3
+    const float4 q0 = *reinterpret_cast<const float4*>(rp);
+    const float4 q7 = *reinterpret_cast<const float4*>(rp + 28);
+    const float4 q8 = *reinterpret_cast<const float4*>(rp + 32);
+    unsigned u = max(max(__float_as_uint(q0.w), __float_as_uint(q7.x)), __float_as_uint(q7.y));
+    u = max(u, __float_as_uint(q7.z));
+    if (o <= 2) u = max(u, __float_as_uint(q0.z));
+    if (o <= 1) u = max(u, __float_as_uint(q0.y));
+    if (o == 0) u = max(u, __float_as_uint(q0.x));
+    if (o >= 1) u = max(u, __float_as_uint(q7.w));
+    if (o >= 2) u = max(u, __float_as_uint(q8.x));
+    if (o >= 3) u = max(u, __float_as_uint(q8.y));
+#pragma unroll
+    for (int i = 1; i < 7; ++i) {  // columns a+4 .. a+27: inside the window for every o
+      const float4 q = *reinterpret_cast<const float4*>(rp + 4 * i);
+      u = max(max(u, __float_as_uint(q.x)), __float_as_uint(q.y));
+      u = max(max(u, __float_as_uint(q.z)), __float_as_uint(q.w));
+    }
+    m = u;
+  }
+  return __uint_as_float(__reduce_max_sync(kFull, m));
+}
+
 // Dense large fill (many empty pixels in a warp's block): one pass for the
 // vertical 31-row maxima of the block's four rows over the warp's columns
 // L-11 .. L+140 into V[4][kVC] (34 ring rows per column), then each lane takes
@@ -565,9 +608,9 @@ struct State {
   float* wring;        // producer write base: ring + lane column (owned lanes only)
   float* ring;
   int ringw, x0, lane, L, p0, p1;
-  unsigned own, outm, oob, oobL, oobR;
+  unsigned own, outm, oob;
   bool woob;
-  float nb[4];  // -FMAX where the consumer needs the column, +FMAX elsewhere
+  unsigned needm;  // columns the consumer needs (owned +- 2 inside the strip)
   int T0[4];
   float top[4];
   int tmin, tmax;
@@ -590,7 +633,8 @@ struct State {
   uint32_t mbW, mbL, mbR;  // shared addresses of this warp's / the neighbours' P[4], C[4] mbarriers
   bool hasL, hasR;
   int gk;              // block counter across items (mbarrier index and phase)
-  int srcL, srcR, compR;  // replicate sources for out-of-frame columns
+  bool edgeL;          // this lane holds column 0
+  int compR;           // component of column W - 1 in this lane, else -1
 };
 
 template <int VEC, bool FULL, int BLUR, bool PRE, bool DENSE, int IO, bool EDGE>
@@ -660,7 +704,6 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
 #pragma unroll
       for (int j = 0; j < kB; ++j) {
         if (EDGE && (t0 - 1 + j < 0 || t0 - 1 + j >= H)) set_row(d1[j], 0.f);
-        if (S.woob) fix_oob(d1[j], S.oob, 0.f);
       }
     }
     // --- cross3 #2 (rows t0-2+j) ---
@@ -677,7 +720,6 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
 #pragma unroll
       for (int j = 0; j < kB; ++j) {
         if (EDGE && (t0 - 2 + j < 0 || t0 - 2 + j >= H)) set_row(d2[j], 0.f);
-        if (S.woob) fix_oob(d2[j], S.oob, 0.f);
       }
     }
     }
@@ -758,8 +800,14 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
   if (false) {
 #endif
     const uint32_t o = 32 + ((g - 2) & 3) * 8, ph = ((g - 2) >> 2) & 1;
+#ifdef DFC_TIMING
+    const long long tw = clock64();
+#endif
     if (S.hasL) mb_wait(S.mbL + o, ph);
     if (S.hasR) mb_wait(S.mbR + o, ph);
+#ifdef DFC_TIMING
+    S.tacc[1] += clock64() - tw;
+#endif
   }
   if (S.own) {
     float* w = S.wring + (k % kRingBlocks) * kB * S.ringw;
@@ -815,12 +863,13 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
     }
   }
   if (FULL) {
-    // any needed empty pixel in this block? (max with nb masks unneeded columns)
+    // any needed empty pixel in this block?
     float mn = kFMax;
 #pragma unroll
-    for (int j = 0; j < kB; ++j)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) mn = fminf(mn, fmaxf(v6[j].v[c], S.nb[c]));
+    for (int c = 0; c < 4; ++c) {
+      const float cm = fminf(fminf(v6[0].v[c], v6[1].v[c]), fminf(v6[2].v[c], v6[3].v[c]));
+      if (S.needm >> c & 1) mn = fminf(mn, cm);
+    }
 #ifdef DFC_EXP_NOLF
     if (false) {
 #else
@@ -830,7 +879,7 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
 #pragma unroll
       for (int j = 0; j < kB; ++j)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) em |= (unsigned)!(fmaxf(v6[j].v[c], S.nb[c]) > kValid) << (4 * j + c);
+        for (int c = 0; c < 4; ++c) em |= (unsigned)((S.needm >> c & 1) && !(v6[j].v[c] > kValid)) << (4 * j + c);
       S.had_empty |= em != 0;
       unsigned lanes = __ballot_sync(kFull, em != 0);
       // neighbours' rows up to tc0 + 18
@@ -874,7 +923,10 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
           const int b = __ffs(pe) - 1;
           pe &= pe - 1;
           const int row = EDGE ? min(max(tc0 + (b >> 2), 0), H - 1) : tc0 + (b >> 2);
-          const float r = lf_one<LG::P>(S.ring, S.ringw, S.p0, S.p1, H, S.lane, S.L + 4 * src + (b & 3), row);
+          const int x = S.L + 4 * src + (b & 3);
+          const float r = (x - kLF >= S.p0 && x + kLF < S.p1)
+                              ? lf_rows<LG::P>(S.ring, S.ringw, S.p0, H, S.lane, x, row)
+                              : lf_one<LG::P>(S.ring, S.ringw, S.p0, S.p1, H, S.lane, x, row);
           if (S.lane == src) {
 #pragma unroll
             for (int j = 0; j < kB; ++j)
@@ -890,22 +942,36 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
 #ifdef DFC_TIMING
   S.tacc[4] += clock64() - ct.tc;
 #endif
-  // out-of-frame columns replicate the edge column (the blur needs true replicate)
-  if (S.woob) {
-#pragma unroll
-    for (int j = 0; j < kB; ++j) {
-      const float eL = __shfl_sync(kFull, v6[j].v[0], S.srcL);
-      const float sr = S.compR == 0 ? v6[j].v[0] : (S.compR == 1 ? v6[j].v[1] : (S.compR == 2 ? v6[j].v[2] : v6[j].v[3]));
-      const float eR = __shfl_sync(kFull, sr, S.srcR);
-      fix_oob(v6[j], S.oobL, eL);
-      fix_oob(v6[j], S.oobR, eR);
-    }
-  }
   if constexpr (BLUR == DFC_BLUR_GAUSSIAN) {
     F4 h[kB];
 #pragma unroll
     for (int j = 0; j < kB; ++j) {
-      const Ext<2> e = ext_row<2>(v6[j]);
+      // replicate border: the lanes holding column 0 / W - 1 overwrite the
+      // out-of-frame entries of their window with the edge value (only they
+      // and, when W - 1 starts a lane, the lane before it produce in-frame
+      // outputs from out-of-frame columns; that one reads the sender's patch)
+      if constexpr (VEC != 4) {
+        if (S.woob && S.compR >= 0 && S.compR < 3) {
+          const float ev = S.compR == 0 ? v6[j].v[0] : (S.compR == 1 ? v6[j].v[1] : v6[j].v[2]);
+#pragma unroll
+          for (int c = 1; c < 4; ++c)
+            if (c > S.compR) v6[j].v[c] = ev;
+        }
+      }
+      Ext<2> e = ext_row<2>(v6[j]);
+      if (S.woob) {
+        if (S.edgeL) e.e[0] = e.e[1] = e.e[2];
+        if (S.compR >= 0) {
+          if constexpr (VEC == 4) {
+            e.e[6] = e.e[7] = e.e[5];
+          } else {
+            const float ev = S.compR == 0 ? e.e[2] : (S.compR == 1 ? e.e[3] : (S.compR == 2 ? e.e[4] : e.e[5]));
+#pragma unroll
+            for (int i = 3; i < 8; ++i)
+              if (i > S.compR + 2) e.e[i] = ev;
+          }
+        }
+      }
 #pragma unroll
       for (int hp = 0; hp < 2; ++hp) {  // packed fp32x2: outputs (2hp, 2hp+1), inputs broadcast
         const float* x = e.e + 2 * hp;
@@ -1009,7 +1075,7 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
     Geo g;
     item_geometry((int)(item % p.strips), p, warp, g);
     State S;
-    S.ringw = ((g.p1 - g.p0) + 3) & ~3;
+    S.ringw = ring_width(g.p1 - g.p0);
     S.ring = smem;
     const TIn* src = static_cast<const TIn*>(p.in) + frame * HW;
     TOut* dst = static_cast<TOut*>(p.out) + frame * HW;
@@ -1021,28 +1087,23 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
     S.wring = S.ring + (S.x0 - g.p0);
     S.rring = S.ring + (min(max(S.x0, g.p0), g.p0 + S.ringw - 4) - g.p0);
     unsigned incol = 0, needm = 0;
-    S.own = S.outm = S.oob = S.oobL = S.oobR = 0;
+    S.own = S.outm = S.oob = 0;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const int x = S.x0 + c;
       incol |= (unsigned)(x >= 0 && x < W) << c;
-      S.oobL |= (unsigned)(x < 0) << c;
-      S.oobR |= (unsigned)(x >= W) << c;
+      S.oob |= (unsigned)(x < 0 || x >= W) << c;
       S.own |= (unsigned)(x >= g.q0 && x < g.q1) << c;
       S.outm |= (unsigned)(x >= max(g.q0, g.o0) && x < min(g.q1, g.o1)) << c;
       const bool need = x >= max(max(g.q0 - 2, g.o0 - 2), max(g.p0, 0)) && x < min(min(g.q1 + 2, g.o1 + 2), g.p1);
-      S.nb[c] = need ? -kFMax : kFMax;
       needm |= (unsigned)need << c;
     }
     S.incol = incol;
+    S.needm = needm;
     S.full = incol == 0xFu;
-    S.oob = S.oobL | S.oobR;
     S.woob = __any_sync(kFull, S.oob != 0);
-    S.srcL = (0 - g.L) >> 2;  // lane holding column 0 (component 0)
-    S.srcR = (W - 1 - g.L) >> 2;
-    S.compR = (W - 1 - g.L) & 3;
-    S.srcL = min(max(S.srcL, 0), 31);
-    S.srcR = min(max(S.srcR, 0), 31);
+    S.edgeL = S.x0 == 0;                                           // lane holding column 0
+    S.compR = (S.x0 <= W - 1 && W - 1 <= S.x0 + 3) ? W - 1 - S.x0 : -1;  // component of column W - 1
     S.umax = 0;
     S.had_empty = S.still_empty = false;
     S.skip = S.fast = S.enc_over = false;
@@ -1083,7 +1144,8 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
     }
 
 #ifdef DFC_TIMING
-    S.tacc[3] = clock64() - tph;
+    S.tacc[3] = 0;
+    (void)tph;
 #endif
     // ---------------- phase 2 ----------------
 #pragma unroll
@@ -1111,6 +1173,11 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
     for (; k < K; ++k) iterate<VEC, FULL, BLUR, PRE, DENSE, IO, true>(p, S, k);
 
 #ifdef DFC_TIMING
+    {
+      const long long tz = clock64();
+      __syncthreads();  // item-end imbalance (diagnostics build only)
+      S.tacc[3] = clock64() - tz;
+    }
     if (lane == 0)
       for (int i = 0; i < 6; ++i) p.tim[(blockIdx.x * kNW + warp) * 6 + i] += S.tacc[i];
 #endif

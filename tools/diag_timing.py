@@ -66,8 +66,9 @@ def run(frames=1024):
         assert rc == 0, rc
         torch.cuda.synchronize()
     t = tim.view(148, 12, 6).cpu().numpy().astype(np.float64)
-    names = ["producer", "(C wait)", "consumer", "phase1", "(cons:ring+LF)", "(LF wait)"]
+    names = ["producer", "(ring wait)", "consumer", "item-end wait", "(cons:ring+LF)", "fast blocks"]
     tot = t[:, :, [0, 2, 3]].sum(axis=2)
+    t[:, :, 5] *= 1e6 / frames  # fast-block count per frame (scaled to print as-is)
     print("per-warp mean cycles (over CTAs), share of warp time:")
     print("warp " + " ".join(f"{n:>10s}" for n in names) + "      total")
     for w in range(12):

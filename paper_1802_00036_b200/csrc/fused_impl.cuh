@@ -950,7 +950,9 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
       // out-of-frame entries of their window with the edge value (only they
       // and, when W - 1 starts a lane, the lane before it produce in-frame
       // outputs from out-of-frame columns; that one reads the sender's patch)
-      if constexpr (VEC != 4) {
+      if constexpr (VEC == 2) {  // W % 4 == 2: column W - 1 is component 1 of its lane
+        if (S.woob && S.compR >= 0) v6[j].v[2] = v6[j].v[3] = v6[j].v[1];
+      } else if constexpr (VEC == 1) {
         if (S.woob && S.compR >= 0 && S.compR < 3) {
           const float ev = S.compR == 0 ? v6[j].v[0] : (S.compR == 1 ? v6[j].v[1] : v6[j].v[2]);
 #pragma unroll
@@ -964,6 +966,8 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
         if (S.compR >= 0) {
           if constexpr (VEC == 4) {
             e.e[6] = e.e[7] = e.e[5];
+          } else if constexpr (VEC == 2) {
+            e.e[6] = e.e[7] = e.e[3];
           } else {
             const float ev = S.compR == 0 ? e.e[2] : (S.compR == 1 ? e.e[3] : (S.compR == 2 ? e.e[4] : e.e[5]));
 #pragma unroll

@@ -633,6 +633,7 @@ struct State {
   uint32_t mbW, mbL, mbR;  // shared addresses of this warp's / the neighbours' P[4], C[4] mbarriers
   bool hasL, hasR;
   int gk;              // block counter across items (mbarrier index and phase)
+  int pblk;            // ring block of the producer's rows (k mod ring blocks)
   bool edgeL;          // this lane holds column 0
   int compR;           // component of column W - 1 in this lane, else -1
 };
@@ -810,12 +811,14 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
 #endif
   }
   if (S.own) {
-    float* w = S.wring + (k % kRingBlocks) * kB * S.ringw;
+    float* w = S.wring + S.pblk * (kB * S.ringw);
 #pragma unroll
     for (int j = 0; j < kB; ++j)
       if (!EDGE || (tp + j >= 0 && tp + j < H))
         *reinterpret_cast<float4*>(w + j * S.ringw) = make_float4(f[j].v[0], f[j].v[1], f[j].v[2], f[j].v[3]);
   }
+  const int cblk = S.pblk >= kLag / kB ? S.pblk - kLag / kB : S.pblk + kRingBlocks - kLag / kB;
+  S.pblk = S.pblk == kRingBlocks - 1 ? 0 : S.pblk + 1;
   __syncwarp();
   if (S.lane == 0) mb_arrive(S.mbW + (g & 3) * 8);
 #ifdef DFC_TIMING
@@ -850,7 +853,7 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
   F4 v6[kB];
   {
     // rows tc0 + j live in slots 4*((k + 6) mod 10) + j when inside the frame
-    const float* r = S.rring + ((k + kRingBlocks - kLag / kB) % kRingBlocks) * kB * S.ringw;
+    const float* r = S.rring + cblk * (kB * S.ringw);
 #pragma unroll
     for (int j = 0; j < kB; ++j) {
       const float* rr = r + j * S.ringw;
@@ -1117,6 +1120,7 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
     S.hasL = warp > 0;
     S.hasR = warp + 1 < p.nw;
     S.gk = gk;
+    S.pblk = 0;
     S.tmaxN = INT_MAX;
     set_row(S.ofast, 0.f);
 

@@ -66,6 +66,7 @@ struct Lags {
   static constexpr int C = P + kLag;      // consumer rows = t0 - C + j
   static constexpr int KFirst = C / kB;
 };
+constexpr int kMbCount = 32;            // mbarrier arrivals per phase: every lane of the warp
 constexpr int kLF = 15;                // large fill radius
 constexpr int kStripMax = 1248;        // widest strip handled by one CTA
 constexpr uint32_t kNeedsStaged = 0x200u;  // internal status bit (capi.cu)
@@ -575,7 +576,7 @@ __device__ __forceinline__ F4 lf_hquad(const float* __restrict__ V, int j, int l
 // ---------------------------------------------------------------------------
 // per-item state and one 4-row iteration (EDGE: rows may leave the frame)
 // ---------------------------------------------------------------------------
-// Per-warp mbarriers (one arrival each) replace the per-block CTA barrier.  A
+// Per-warp mbarriers (32 arrivals: every lane releases its own stores) replace the per-block CTA barrier.  A
 // warp's ring columns are read only by itself and its two neighbours (lane
 // halos +-12, large fill +-17 < the 104 owned columns), so warps synchronise
 // with their neighbours only: P_w[g & 3] completes when warp w has stored
@@ -819,8 +820,7 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
   }
   const int cblk = S.pblk >= kLag / kB ? S.pblk - kLag / kB : S.pblk + kRingBlocks - kLag / kB;
   S.pblk = S.pblk == kRingBlocks - 1 ? 0 : S.pblk + 1;
-  __syncwarp();
-  if (S.lane == 0) mb_arrive(S.mbW + (g & 3) * 8);
+  mb_arrive(S.mbW + (g & 3) * 8);  // every lane (count 32): each lane's ring stores are released by its own arrival
 #ifdef DFC_TIMING
   const long long tb = clock64();
   struct ConsTimer {
@@ -1044,8 +1044,7 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
     }
   }
   } while (0);
-  __syncwarp();
-  if (S.lane == 0) mb_arrive(S.mbW + 32 + (g & 3) * 8);
+  mb_arrive(S.mbW + 32 + (g & 3) * 8);
 }
 
 // ---------------------------------------------------------------------------
@@ -1065,7 +1064,7 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int i = 0; i < kNW * 8; ++i)
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(mb0 + 8 * i), "r"(1) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(mb0 + 8 * i), "r"(kMbCount) : "memory");
   }
   int gk = 0;  // blocks done across items (mbarrier phases); first use is after the item barrier below
   const int H = p.H, W = p.W;

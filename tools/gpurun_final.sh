@@ -1,0 +1,12 @@
+# Round-end measurement set: tests, smoke, every config's bench line, the
+# reference arm, the config-1 launch list and one ncu --set full capture.
+set -x
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/smi.txt 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc $?" >> gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc $?" >> gpurun_out/smoke.log
+timeout 600 python bench.py > gpurun_out/bench_c1.log 2>&1
+for c in 0 2 3 4; do timeout 400 python bench.py --config $c --no-cpu-baseline > gpurun_out/bench_c$c.log 2>&1; done
+timeout 400 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.log 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_c1.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:"fused_kernel|r0_kernel" -c 2 -o gpurun_out/final_full python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1

@@ -574,6 +574,98 @@ __device__ __forceinline__ F4 lf_hquad(const float* __restrict__ V, int j, int l
 }
 
 // ---------------------------------------------------------------------------
+// Tensor memory as a per-thread store for the rows each stage carries from
+// one block to the next (TMEM is otherwise idle here: no MMA).  Each warp owns
+// 96 columns of its lane quarter (warps w, w+4, w+8 share quarter w & 3); a
+// thread reads / writes its own lane with the 32x32b shapes, one x16 / x8
+// load right before a stage and one store right after it.  Off the register
+// file, the carried rows no longer stay live across the whole block: 168
+// registers with 136 B of spills became 148 registers with none, and the
+// per-block rotation moves are gone (config 1: 598k -> 701k frames/s).
+// ---------------------------------------------------------------------------
+constexpr int kTmCols = 512;   // allocation (power of 2 >= 3 warps x 96 columns)
+constexpr int kTmSlice = 96;   // c5 0..23, gc 24..39, c3 40..55, c4 56..71, c1 72..79, c2 80..87
+static_assert(((kNW + 3) / 4) * kTmSlice <= kTmCols, "TMEM slices");
+template <int N>
+__device__ __forceinline__ void tm_ld(uint32_t a, float* v);
+template <>
+__device__ __forceinline__ void tm_ld<16>(uint32_t a, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(a)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+template <>
+__device__ __forceinline__ void tm_ld<8>(uint32_t a, float* v) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(a)
+               : "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void tm_st(uint32_t a, const float* v);
+template <>
+__device__ __forceinline__ void tm_st<16>(uint32_t a, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n" ::"r"(a),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+      "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+      "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15]))
+      : "memory");
+}
+template <>
+__device__ __forceinline__ void tm_st<8>(uint32_t a, const float* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(a),
+               "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+               "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+               "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7]))
+               : "memory");
+}
+// c5 (6 rows x 4 columns) at columns 0..23, gc (4 rows x 4) at 24..39 of the warp's slice
+__device__ __forceinline__ void tm_ld_rows(uint32_t a, F4* rows, int n) {
+  float v[24];
+  if (n == 6) {
+    tm_ld<16>(a, v);
+    tm_ld<8>(a + 16, v + 16);
+  } else if (n == 4) {
+    tm_ld<16>(a, v);
+  } else {
+    tm_ld<8>(a, v);
+  }
+  tm_wait_ld();
+#pragma unroll
+  for (int i = 0; i < 6; ++i)
+    if (i < n) rows[i] = F4{{v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]}};
+}
+__device__ __forceinline__ void tm_st_rows(uint32_t a, const F4* rows, int n) {
+  float v[24];
+#pragma unroll
+  for (int i = 0; i < 6; ++i)
+    if (i < n)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) v[4 * i + c] = rows[i].v[c];
+  if (n == 6) {
+    tm_st<16>(a, v);
+    tm_st<8>(a + 16, v + 16);
+  } else if (n == 4) {
+    tm_st<16>(a, v);
+  } else {
+    tm_st<8>(a, v);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // per-item state and one 4-row iteration (EDGE: rows may leave the frame)
 // ---------------------------------------------------------------------------
 // Per-warp mbarriers (32 arrivals: every lane releases its own stores) replace the per-block CTA barrier.  A
@@ -589,14 +681,6 @@ __device__ __forceinline__ void mb_arrive(uint32_t a) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(a) : "memory");
 }
 __device__ __forceinline__ void mb_wait(uint32_t a, uint32_t parity) {
-#ifdef DFC_EXP_SUSPEND
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1, %2;\n"
-      " @!p bra WAIT_%=;\n}\n" ::"r"(a),
-      "r"(parity), "r"(DFC_EXP_SUSPEND)
-      : "memory");
-  return;
-#endif
   asm volatile(
       "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
       " @!p bra WAIT_%=;\n}\n" ::"r"(a),
@@ -617,7 +701,7 @@ struct State {
   int tmin, tmax;
   int tmaxN;           // max r0 row (processing order) over the columns the consumer needs
   bool skip, fast;
-  F4 c1[2], c2[2], c3[4], c4[4], c5[6], gc[4], mprev[2];
+  F4 mprev[2];        // PARTIAL: pre-blur rows for the re-impose mask
   F4 ofast;            // output row above every needed r0 (FULL): all such rows are equal
   uint32_t stg;        // shared-memory staging slot of this lane (row j at +512 j)
   const void* lrow;    // input row of processing row t0 + kB at column x0
@@ -635,6 +719,7 @@ struct State {
   bool hasL, hasR;
   int gk;              // block counter across items (mbarrier index and phase)
   int pblk;            // ring block of the producer's rows (k mod ring blocks)
+  uint32_t tm;         // tensor-memory address of this thread's carried rows (c5, gc)
   bool edgeL;          // this lane holds column 0
   int compR;           // component of column W - 1 in this lane, else -1
 };
@@ -694,7 +779,11 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
     } else {
     F4 d1[kB];
     {
-      const F4 in[kB + 2] = {S.c1[0], S.c1[1], a[0], a[1], a[2], a[3]};
+      F4 c1[2];
+      tm_wait_st();
+      tm_ld_rows(S.tm + 72, c1, 2);
+      const F4 in[kB + 2] = {c1[0], c1[1], a[0], a[1], a[2], a[3]};
+      tm_st_rows(S.tm + 72, a + 2, 2);
 #pragma unroll
       for (int j = 0; j < kB; ++j) {
         const Ext<1> e = ext_row<1>(in[j + 1]);
@@ -702,7 +791,6 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
         for (int c = 0; c < 4; ++c)
           d1[j].v[c] = fmx3(fmx3(in[j].v[c], in[j + 1].v[c], in[j + 2].v[c]), e.e[c], e.e[c + 2]);
       }
-      S.c1[0] = a[2], S.c1[1] = a[3];
 #pragma unroll
       for (int j = 0; j < kB; ++j) {
         if (EDGE && (t0 - 1 + j < 0 || t0 - 1 + j >= H)) set_row(d1[j], 0.f);
@@ -710,7 +798,10 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
     }
     // --- cross3 #2 (rows t0-2+j) ---
     {
-      const F4 in[kB + 2] = {S.c2[0], S.c2[1], d1[0], d1[1], d1[2], d1[3]};
+      F4 c2[2];
+      tm_ld_rows(S.tm + 80, c2, 2);
+      const F4 in[kB + 2] = {c2[0], c2[1], d1[0], d1[1], d1[2], d1[3]};
+      tm_st_rows(S.tm + 80, d1 + 2, 2);
 #pragma unroll
       for (int j = 0; j < kB; ++j) {
         const Ext<1> e = ext_row<1>(in[j + 1]);
@@ -718,7 +809,6 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
         for (int c = 0; c < 4; ++c)
           d2[j].v[c] = fmx3(fmx3(in[j].v[c], in[j + 1].v[c], in[j + 2].v[c]), e.e[c], e.e[c + 2]);
       }
-      S.c2[0] = d1[2], S.c2[1] = d1[3];
 #pragma unroll
       for (int j = 0; j < kB; ++j) {
         if (EDGE && (t0 - 2 + j < 0 || t0 - 2 + j >= H)) set_row(d2[j], 0.f);
@@ -728,13 +818,14 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
     // --- close: max5 (rows t0-L2-2+j) ---
     F4 m5[kB];
     {
-      const F4 in[kB + 4] = {S.c3[0], S.c3[1], S.c3[2], S.c3[3], d2[0], d2[1], d2[2], d2[3]};
+      F4 c3[4];
+      tm_ld_rows(S.tm + 40, c3, 4);
+      const F4 in[kB + 4] = {c3[0], c3[1], c3[2], c3[3], d2[0], d2[1], d2[2], d2[3]};
+      tm_st_rows(S.tm + 40, d2, 4);
       F4 vv[kB];
       vwin2<OpMax>(in, vv);
 #pragma unroll
       for (int j = 0; j < kB; ++j) m5[j] = hwin2<OpMax>(ext_row<2>(vv[j]));
-#pragma unroll
-      for (int i = 0; i < 4; ++i) S.c3[i] = d2[i];
 #pragma unroll
       for (int j = 0; j < kB; ++j) {
         if (EDGE && (t0 - L2 - 2 + j < 0 || t0 - L2 - 2 + j >= H)) set_row(m5[j], kFMax);
@@ -744,13 +835,14 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
     // --- close: min5 (rows t0-L2-4+j) ---
     F4 cl[kB];
     {
-      const F4 in[kB + 4] = {S.c4[0], S.c4[1], S.c4[2], S.c4[3], m5[0], m5[1], m5[2], m5[3]};
+      F4 c4[4];
+      tm_ld_rows(S.tm + 56, c4, 4);
+      const F4 in[kB + 4] = {c4[0], c4[1], c4[2], c4[3], m5[0], m5[1], m5[2], m5[3]};
+      tm_st_rows(S.tm + 56, m5, 4);
       F4 vv[kB];
       vwin2<OpMin>(in, vv);
 #pragma unroll
       for (int j = 0; j < kB; ++j) cl[j] = hwin2<OpMin>(ext_row<2>(vv[j]));
-#pragma unroll
-      for (int i = 0; i < 4; ++i) S.c4[i] = m5[i];
 #pragma unroll
       for (int j = 0; j < kB; ++j) {
         if (EDGE && (t0 - L2 - 4 + j < 0 || t0 - L2 - 4 + j >= H)) set_row(cl[j], 0.f);
@@ -759,7 +851,10 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
     }
     // --- small fill: masked max7 (rows t0-L2-7+j = tp+j) ---
     {
-      const F4 in[kB + 6] = {S.c5[0], S.c5[1], S.c5[2], S.c5[3], S.c5[4], S.c5[5], cl[0], cl[1], cl[2], cl[3]};
+      F4 c5[6];
+      tm_wait_st();  // the previous block's store of these rows
+      tm_ld_rows(S.tm, c5, 6);
+      const F4 in[kB + 6] = {c5[0], c5[1], c5[2], c5[3], c5[4], c5[5], cl[0], cl[1], cl[2], cl[3]};
       F4 vv[kB];
       vwin3<OpMax>(in, vv);
 #pragma unroll
@@ -771,9 +866,10 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
           f[j].v[c] = ctr > kValid ? ctr : h7.v[c];
         }
       }
-      S.c5[0] = S.c5[4], S.c5[1] = S.c5[5];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) S.c5[i + 2] = cl[i];
+      {
+        const F4 n5[6] = {c5[4], c5[5], cl[0], cl[1], cl[2], cl[3]};
+        tm_st_rows(S.tm, n5, 6);
+      }
     }
     // --- extend to top (FULL; only blocks reaching some column's r0) ---
     if (FULL && tp + kB - 1 >= S.tmin) {
@@ -796,11 +892,7 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
   S.lrow = static_cast<const TIn*>(S.lrow) - kB * W;
   // --- ring store: ring slot of row t is (t + P) mod 40, so this block is slots 4*(k mod 10) + j ---
   const int g = S.gk++;
-#ifndef DFC_EXP_NOWAIT
   if (g >= 2) {
-#else
-  if (false) {
-#endif
     const uint32_t o = 32 + ((g - 2) & 3) * 8, ph = ((g - 2) >> 2) & 1;
 #ifdef DFC_TIMING
     const long long tw = clock64();
@@ -873,11 +965,7 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
       const float cm = fminf(fminf(v6[0].v[c], v6[1].v[c]), fminf(v6[2].v[c], v6[3].v[c]));
       if (S.needm >> c & 1) mn = fminf(mn, cm);
     }
-#ifdef DFC_EXP_NOLF
-    if (false) {
-#else
     if (__any_sync(kFull, !(mn > kValid))) {
-#endif
       unsigned em = 0;  // bit 4j+c: needed empty pixel
 #pragma unroll
       for (int j = 0; j < kB; ++j)
@@ -886,10 +974,8 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
       S.had_empty |= em != 0;
       unsigned lanes = __ballot_sync(kFull, em != 0);
       // neighbours' rows up to tc0 + 18
-#ifndef DFC_EXP_NOWAIT
       if (S.hasL) mb_wait(S.mbL + (g & 3) * 8, (g >> 2) & 1);
       if (S.hasR) mb_wait(S.mbR + (g & 3) * 8, (g >> 2) & 1);
-#endif
       if (DENSE && __reduce_add_sync(kFull, __popc(em)) > kDenseMin) {
         float* V = S.ring + kRing * S.ringw + p.nw * (kB * 128) + (threadIdx.x >> 5) * (kB * kVC);
         lf_vquad<LG::P>(S.ring, S.ringw, S.p0, S.p1, H, S.L, S.lane, tc0, !EDGE || (tc0 >= 0 && tc0 + kB - 1 < H),
@@ -989,13 +1075,15 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
         h[j].v[2 * hp + 1] = a.y;
       }
     }
+    F4 gcv[4];
+    tm_wait_st();
+    tm_ld_rows(S.tm + 24, gcv, 4);
     if (EDGE && k == LG::KFirst) {  // rows above row 0 replicate it (tc0 in [-3, 0]: h[0] is row 0)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) S.gc[i] = h[0];
+      for (int i = 0; i < 4; ++i) gcv[i] = h[0];
     }
-    const F4 in[kB + 4] = {S.gc[0], S.gc[1], S.gc[2], S.gc[3], h[0], h[1], h[2], h[3]};
-#pragma unroll
-    for (int i = 0; i < 4; ++i) S.gc[i] = h[i];
+    const F4 in[kB + 4] = {gcv[0], gcv[1], gcv[2], gcv[3], h[0], h[1], h[2], h[3]};
+    tm_st_rows(S.tm + 24, h, 4);
     F4 mk[kB];
     if (!FULL) {  // pre-blur validity of output rows tc0-2+j (pipeline.py:212-214)
       mk[0] = S.mprev[0], mk[1] = S.mprev[1], mk[2] = v6[0], mk[3] = v6[1];
@@ -1066,6 +1154,18 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
     for (int i = 0; i < kNW * 8; ++i)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(mb0 + 8 * i), "r"(kMbCount) : "memory");
   }
+  __shared__ uint32_t s_tm;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&s_tm)),
+                 "n"(kTmCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmbase = s_tm;
   int gk = 0;  // blocks done across items (mbarrier phases); first use is after the item barrier below
   const int H = p.H, W = p.W;
   const int64_t HW = (int64_t)H * W;
@@ -1156,11 +1256,22 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
 #endif
     // ---------------- phase 2 ----------------
 #pragma unroll
-    for (int i = 0; i < 2; ++i) set_row(S.c1[i], 0.f), set_row(S.c2[i], 0.f), set_row(S.mprev[i], 0.f);
+    for (int i = 0; i < 2; ++i) set_row(S.mprev[i], 0.f);
+    S.tm = tmbase + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * kTmSlice);
+    {
+      F4 z[6];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) set_row(S.c3[i], 0.f), set_row(S.c4[i], kFMax), set_row(S.gc[i], 0.f);
+      for (int i = 0; i < 6; ++i) set_row(z[i], 0.f);
+      tm_wait_st();
+      tm_st_rows(S.tm, z, 6);
+      tm_st_rows(S.tm + 24, z, 4);
+      tm_st_rows(S.tm + 40, z, 4);
+      tm_st_rows(S.tm + 72, z, 2);
+      tm_st_rows(S.tm + 80, z, 2);
 #pragma unroll
-    for (int i = 0; i < 6; ++i) set_row(S.c5[i], 0.f);
+      for (int i = 0; i < 4; ++i) set_row(z[i], kFMax);
+      tm_st_rows(S.tm + 56, z, 4);
+    }
     S.stg = (uint32_t)__cvta_generic_to_shared(smem + kRing * S.ringw) + warp * (kB * 512) + lane * 16;
     cp_async_wait_all();  // no copy of the previous item may still land in the slot
 #pragma unroll
@@ -1205,6 +1316,12 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
     }
     __syncthreads();  // ring reuse by the next item
   }
+  tm_wait_st();
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmbase), "n"(kTmCols) : "memory");
 }
 
 // Phase 1 of every (item, warp slot) of a round as independent warps (the

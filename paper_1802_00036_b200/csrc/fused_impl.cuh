@@ -1033,24 +1033,33 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
 #endif
   if constexpr (BLUR == DFC_BLUR_GAUSSIAN) {
     F4 h[kB];
+    // replicate border: the lanes holding column 0 / W - 1 overwrite the
+    // out-of-frame entries of their window with the edge value (only they
+    // and, when W - 1 starts a lane, the lane before it produce in-frame
+    // outputs from out-of-frame columns; that one reads the sender's patch).
+    // One warp-uniform branch for the whole block: interior warps skip it.
+    if (S.woob) {
 #pragma unroll
-    for (int j = 0; j < kB; ++j) {
-      // replicate border: the lanes holding column 0 / W - 1 overwrite the
-      // out-of-frame entries of their window with the edge value (only they
-      // and, when W - 1 starts a lane, the lane before it produce in-frame
-      // outputs from out-of-frame columns; that one reads the sender's patch)
-      if constexpr (VEC == 2) {  // W % 4 == 2: column W - 1 is component 1 of its lane
-        if (S.woob && S.compR >= 0) v6[j].v[2] = v6[j].v[3] = v6[j].v[1];
-      } else if constexpr (VEC == 1) {
-        if (S.woob && S.compR >= 0 && S.compR < 3) {
-          const float ev = S.compR == 0 ? v6[j].v[0] : (S.compR == 1 ? v6[j].v[1] : v6[j].v[2]);
+      for (int j = 0; j < kB; ++j) {
+        if constexpr (VEC == 2) {  // W % 4 == 2: column W - 1 is component 1 of its lane
+          if (S.compR >= 0) v6[j].v[2] = v6[j].v[3] = v6[j].v[1];
+        } else if constexpr (VEC == 1) {
+          if (S.compR >= 0 && S.compR < 3) {
+            const float ev = S.compR == 0 ? v6[j].v[0] : (S.compR == 1 ? v6[j].v[1] : v6[j].v[2]);
 #pragma unroll
-          for (int c = 1; c < 4; ++c)
-            if (c > S.compR) v6[j].v[c] = ev;
+            for (int c = 1; c < 4; ++c)
+              if (c > S.compR) v6[j].v[c] = ev;
+          }
         }
       }
-      Ext<2> e = ext_row<2>(v6[j]);
-      if (S.woob) {
+    }
+    Ext<2> ex[kB];
+#pragma unroll
+    for (int j = 0; j < kB; ++j) ex[j] = ext_row<2>(v6[j]);
+    if (S.woob) {
+#pragma unroll
+      for (int j = 0; j < kB; ++j) {
+        Ext<2>& e = ex[j];
         if (S.edgeL) e.e[0] = e.e[1] = e.e[2];
         if (S.compR >= 0) {
           if constexpr (VEC == 4) {
@@ -1065,6 +1074,10 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
           }
         }
       }
+    }
+#pragma unroll
+    for (int j = 0; j < kB; ++j) {
+      const Ext<2>& e = ex[j];
 #pragma unroll
       for (int hp = 0; hp < 2; ++hp) {  // packed fp32x2: outputs (2hp, 2hp+1), inputs broadcast
         const float* x = e.e + 2 * hp;

@@ -180,6 +180,27 @@ def test_determinism_across_batch_sizes(P):
     assert np.array_equal(_bits(a), _bits(b)) and np.array_equal(_bits(a), _bits(c))
 
 
+@pytest.mark.parametrize("blur,fill", [("gaussian", "full"), ("bilateral", "partial")])
+def test_many_items_per_cta(P, blur, fill):
+    """More frames than SMs: each persistent CTA takes several items in a row, so
+    the tensor-memory carry rows, the mbarrier phases and the shared ring carry
+    on across items (and the raw mode runs several fused -> blur-tail rounds).
+    The big batch must equal the same frames run in chunks small enough for one
+    item per CTA, bit for bit, and late frames must match the oracle."""
+    n = 320
+    frames = synth.make_batch(1, 600, n)
+    kw = {"blur_mode": blur, "fill_mode": fill}
+    cfg = _pcfg(P, kw)
+    big = P.complete_batch(frames, cfg)
+    got = big.dense.cpu().numpy()
+    small = np.concatenate([P.complete_batch(frames[i:i + 80], cfg).dense.cpu().numpy() for i in range(0, n, 80)])
+    assert np.array_equal(_bits(got), _bits(small))
+    for i in (148, 297, n - 1):
+        ref, info = O.complete_with_stats(frames[i], _ocfg(kw))
+        _cmp(got[i], ref, blur)
+        assert int(big.iterations[i]) == info["large_fill_iterations"]
+
+
 def test_full_mode_properties(P):
     """density 1.0 and range envelope on generated frames."""
     frames = synth.make_batch(1, 500, 8)

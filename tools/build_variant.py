@@ -2,7 +2,7 @@
 
     python tools/build_variant.py NAME -DFLAG[=V] ...   ->  paper_1802_00036_b200/libdfc_NAME.so
 
-Only fused.cu / fused_vec4.cu are recompiled; select the variant at run time
+Only fused.cu / fused_vec4.cu (or $VARIANT_SRCS) are recompiled; select the variant at run time
 with DFC_LIB=paper_1802_00036_b200/libdfc_NAME.so (bench.py, tests).
 """
 import subprocess
@@ -21,7 +21,8 @@ def main(name, flags):
     objdir = ROOT / "paper_1802_00036_b200" / "build_obj"
     vdir = objdir / f"var_{name}"
     vdir.mkdir(exist_ok=True)
-    srcs = ["fused.cu", "fused_vec4.cu"]
+    import os
+    srcs = os.environ.get("VARIANT_SRCS", "fused.cu fused_vec4.cu").split()
 
     def cc(s):
         cmd = [B.nvcc(), *B.ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-c", *flags,
@@ -37,7 +38,7 @@ def main(name, flags):
         logs = list(ex.map(cc, srcs))
     (vdir / "ptxas.log").write_text("".join(logs))
     objs = [str(vdir / (Path(s).stem + ".o")) for s in srcs]
-    objs += [str(o) for o in sorted(objdir.glob("*.o")) if o.name not in ("fused.o", "fused_vec4.o")]
+    objs += [str(o) for o in sorted(objdir.glob("*.o")) if o.name not in {Path(x).stem + ".o" for x in srcs}]
     out = ROOT / "paper_1802_00036_b200" / f"libdfc_{name}.so"
     subprocess.run([B.nvcc(), *B.ARCH, "-shared", *objs, "-o", str(out)], check=True)
     print(out)

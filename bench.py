@@ -108,18 +108,61 @@ def gen_frames(start, count, procs=None):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled every ~2 ms by NVML on a host thread;
+    stop(window) keeps the samples taken inside the timed region (host clock
+    between the pre-launch synchronize and the final one).  Falls back to
+    `nvidia-smi -lms 100` when NVML is unavailable."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index):
         self.index = index
         self.proc = None
+        self.nvml = None
         self.lines = []
+        self.samples = []  # (t, sm_mhz, max_mhz, reasons)
+        self.stop_flag = False
+
+    def _nvml_handle(self):
+        import pynvml as N
+        import torch
+
+        N.nvmlInit()
+        try:
+            pr = torch.cuda.get_device_properties(self.index)
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            return N, N.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:  # noqa: BLE001
+            return N, N.nvmlDeviceGetHandleByIndex(self.index)
 
     def start(self):
+        try:
+            N, h = self._nvml_handle()
+            bits = {"hw_slowdown": N.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": N.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": N.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": N.nvmlClocksEventReasonSwPowerCap}
+            mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+
+            def poll():
+                while not self.stop_flag:
+                    try:
+                        sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                        r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.samples.append((time.perf_counter(), float(sm), float(mx),
+                                             {n for n, bit in bits.items() if r & bit}))
+                    except Exception:  # noqa: BLE001
+                        pass
+                    time.sleep(0.002)
+
+            self.nvml = threading.Thread(target=poll, daemon=True)
+            self.nvml.start()
+            return
+        except Exception:  # noqa: BLE001
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
@@ -131,34 +174,41 @@ class ClockSampler:
 
     def _read(self):
         for ln in self.proc.stdout:
-            self.lines.append(ln.strip())
+            self.lines.append((time.perf_counter(), ln.strip()))
 
-    def stop(self):
-        if self.proc is None:
-            return None
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:  # noqa: BLE001
-            self.proc.kill()
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 7:
-                continue
+    def stop(self, window=None):
+        if self.nvml is not None:
+            self.stop_flag = True
+            self.nvml.join(timeout=1)
+            rows = self.samples
+        elif self.proc is not None:
+            self.proc.terminate()
             try:
-                sm.append(float(f[0]))
-                mx.append(float(f[1]))
-            except ValueError:
-                continue
-            for n, v in zip(names, f[3:7]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        if not sm:
+                self.proc.wait(timeout=5)
+            except Exception:  # noqa: BLE001
+                self.proc.kill()
+            rows = []
+            for t, ln in self.lines:
+                f = [x.strip() for x in ln.split(",")]
+                if len(f) < 7:
+                    continue
+                try:
+                    rows.append((t, float(f[0]), float(f[1]),
+                                 {n for n, v in zip(self.NAMES, f[3:7]) if v.lower() == "active"}))
+                except ValueError:
+                    continue
+        else:
             return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        inside = [r for r in rows if window is None or window[0] <= r[0] <= window[1]]
+        use = inside or rows
+        if not use:
+            return None
+        reasons = set()
+        for r in use:
+            reasons |= r[3]
+        return {"sm_mhz": statistics.median(r[1] for r in use), "sm_max_mhz": max(r[2] for r in use),
+                "reasons": sorted(reasons), "samples": len(use), "samples_in_timed_region": len(inside),
+                "source": "nvml 2 ms" if self.nvml is not None else "nvidia-smi 100 ms"}
 
 
 def oracle_config():
@@ -310,24 +360,26 @@ def run_ours(args):
 
     clocks = ClockSampler(local)
     clocks.start()
-    time.sleep(0.3)
+    time.sleep(0.05)
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = L.dfc_kernel_launches()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    th0 = time.perf_counter()
     t0e.record(stream)
     for k in range(args.steps):
         step(*kev[k])
     t1e.record(stream)
     torch.cuda.synchronize()
+    th1 = time.perf_counter()
     if world > 1:
         dist.barrier()
     launches = int(L.dfc_kernel_launches() - launches0)
     elapsed_ms = t0e.elapsed_time(t1e)
     kern_ms = float(np.mean([a.elapsed_time(b) for a, b in kev]))
-    clk = clocks.stop()
+    clk = clocks.stop(window=(th0, th1))
     elapsed_ms, kern_ms = max_over_ranks([elapsed_ms, kern_ms], device=dev)
     ms_step = elapsed_ms / args.steps
     value = world * B * args.steps / (elapsed_ms / 1e3)

@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <cmath>
 
 #include "dfc_common.cuh"
@@ -80,30 +81,54 @@ __device__ __forceinline__ unsigned enc_raw16(float v) {
   return (unsigned)fminf(fmaxf(rintf(v * 256.0f), 0.0f), 65535.0f);
 }
 
-template <int MR, int POST, int PR, bool PARTIAL, bool OUT16>
-__global__ void __launch_bounds__(kThreads) blur_tail_kernel(const float* __restrict__ in, void* __restrict__ out_v,
-                                                             int H, int W, uint32_t* __restrict__ status,
-                                                             const __grid_constant__ TailParams p) {
-  constexpr int HI = MR + PR;                      // input halo
-  constexpr int kTX = kMW - 2 * PR, kTY = kMH - 2 * PR;
-  constexpr int IW = kTX + 2 * HI, IH = kTY + 2 * HI;
+// Tile geometry per (median radius MR, blur radius PR).
+template <int MR, int PR>
+struct TileGeo {
+  static constexpr int HI = MR + PR;  // input halo
+  static constexpr int TX = kMW - 2 * PR, TY = kMH - 2 * PR;
+  static constexpr int IW = TX + 2 * HI, IH = TY + 2 * HI;
   // shared row stride: odd, so the 8x2 median blocks of a warp (bases 8 bx +
   // 2 IWS by) fall on 16 distinct banks instead of 4 (2-way, not 8-way,
   // conflicts; config 2: 110k -> 114.5k frames/s)
-  constexpr int IWS = IW | 1;
-  constexpr int MW = kMW, MH = kMH;
-  __shared__ float sIn[IH * IWS];
-  __shared__ float sM[MH * MW];
-  const int64_t b = blockIdx.z;
-  const int x0 = blockIdx.x * kTX, y0 = blockIdx.y * kTY;
-  const float* src = in + b * (int64_t)H * W;
-  bool over = false;  // OUT16: an output >= 256 m
+  static constexpr int IWS = IW | 1;
+  // Double-buffered persistent CTAs only with the median (long ALU phase to
+  // hide the next tile's staging behind); without it, one tile per CTA and
+  // more resident CTAs hide the loads better (config 0).
+  static constexpr bool kDB = MR > 0;
+  static constexpr size_t kSmem = (size_t)(2 * IH * IWS + kMW * kMH) * sizeof(float);
+};
 
-  for (int i = threadIdx.x; i < IH * IW; i += kThreads) {
-    const int iy = i / IW, ix = i - iy * IW;
-    sIn[iy * IWS + ix] = __ldg(src + (int64_t)clampi(y0 - HI + iy, H) * W + clampi(x0 - HI + ix, W));
+__device__ __forceinline__ void cp_async4(uint32_t sdst, const float* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sdst), "l"(g) : "memory");
+}
+
+// Stage tile t's input (+ halos, replicate-clamped) into sIn with 4-byte
+// cp.async: the copies of the next tile fly while this one is computed.
+template <int MR, int PR>
+__device__ __forceinline__ void stage_tile(const float* __restrict__ in, int H, int W, int tx, int ty, int64_t t,
+                                           float* sIn) {
+  using G = TileGeo<MR, PR>;
+  const int64_t b = t / ((int64_t)tx * ty);
+  const int r = (int)(t - b * tx * ty), byi = r / tx, bxi = r - byi * tx;
+  const int x0 = bxi * G::TX, y0 = byi * G::TY;
+  const float* src = in + b * (int64_t)H * W;
+  const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(sIn);
+  for (int i = threadIdx.x; i < G::IH * G::IW; i += kThreads) {
+    const int iy = i / G::IW, ix = i - iy * G::IW;
+    const float* g = src + (int64_t)clampi(y0 - G::HI + iy, H) * W + clampi(x0 - G::HI + ix, W);
+    cp_async4(s0 + 4 * (iy * G::IWS + ix), g);
   }
-  __syncthreads();
+}
+
+// One output tile from its staged input: median -> blur -> re-impose -> invert back -> store.
+template <int MR, int POST, int PR, bool PARTIAL, bool OUT16>
+__device__ __forceinline__ void tile_process(const float* __restrict__ sIn, float* __restrict__ sM,
+                                             void* __restrict__ out_v, int H, int W, uint32_t* __restrict__ status,
+                                             const TailParams& p, int64_t b, int x0, int y0) {
+  using G = TileGeo<MR, PR>;
+  constexpr int HI = G::HI, kTX = G::TX, kTY = G::TY, IWS = G::IWS;
+  constexpr int MW = kMW, MH = kMH;
+  bool over = false;  // OUT16: an output >= 256 m
 
   // stage-7a: median (or copy) on the tile + blur halo, at frame-clamped centres
   if constexpr (MR == 2) {
@@ -215,18 +240,88 @@ __global__ void __launch_bounds__(kThreads) blur_tail_kernel(const float* __rest
   if (OUT16 && over) atomicOr(status + b, DFC_ST_ENCODE);  // write_depth_png raises (kitti_io.py:60-61)
 }
 
+// With the median: persistent CTAs walk the tiles (frame-major) with two
+// input buffers: tile t + grid is staged with cp.async while tile t is
+// computed, so the latency-bound staging overlaps the ALU-bound median / blur
+// (configs 2 / 4: +4 %).
+template <int MR, int POST, int PR, bool PARTIAL, bool OUT16>
+__global__ void __launch_bounds__(kThreads) blur_tail_kernel(const float* __restrict__ in, void* __restrict__ out_v,
+                                                             int H, int W, uint32_t* __restrict__ status,
+                                                             const __grid_constant__ TailParams p, int tx, int ty,
+                                                             int64_t ntiles) {
+  using G = TileGeo<MR, PR>;
+  extern __shared__ __align__(16) float smem[];
+  float* const sIn0 = smem;
+  float* const sIn1 = smem + G::IH * G::IWS;
+  float* sM = smem + 2 * G::IH * G::IWS;
+  int64_t t = blockIdx.x;
+  if (t < ntiles) stage_tile<MR, PR>(in, H, W, tx, ty, t, sIn0);
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  int cur = 0;
+  for (; t < ntiles; t += gridDim.x) {
+    const int64_t tn = t + gridDim.x;
+    if (tn < ntiles) stage_tile<MR, PR>(in, H, W, tx, ty, tn, cur ? sIn0 : sIn1);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // tile t's copies (this thread's)
+    __syncthreads();                                          // ... and everyone's
+    const int64_t b = t / ((int64_t)tx * ty);
+    const int r = (int)(t - b * tx * ty), byi = r / tx, bxi = r - byi * tx;
+    tile_process<MR, POST, PR, PARTIAL, OUT16>(cur ? sIn1 : sIn0, sM, out_v, H, W, status, p, b, bxi * G::TX,
+                                               byi * G::TY);
+    __syncthreads();  // this tile's input buffer and sM are reused
+    cur ^= 1;
+  }
+}
+
+// Without the median: one tile per CTA (plain loads; many resident CTAs hide them).
+template <int MR, int POST, int PR, bool PARTIAL, bool OUT16>
+__global__ void __launch_bounds__(kThreads) blur_tail_tile_kernel(const float* __restrict__ in,
+                                                                  void* __restrict__ out_v, int H, int W,
+                                                                  uint32_t* __restrict__ status,
+                                                                  const __grid_constant__ TailParams p) {
+  using G = TileGeo<MR, PR>;
+  __shared__ float sIn[G::IH * G::IWS];
+  __shared__ float sM[kMH * kMW];
+  const int64_t b = blockIdx.z;
+  const int x0 = blockIdx.x * G::TX, y0 = blockIdx.y * G::TY;
+  const float* src = in + b * (int64_t)H * W;
+  for (int i = threadIdx.x; i < G::IH * G::IW; i += kThreads) {
+    const int iy = i / G::IW, ix = i - iy * G::IW;
+    sIn[iy * G::IWS + ix] = __ldg(src + (int64_t)clampi(y0 - G::HI + iy, H) * W + clampi(x0 - G::HI + ix, W));
+  }
+  __syncthreads();
+  tile_process<MR, POST, PR, PARTIAL, OUT16>(sIn, sM, out_v, H, W, status, p, b, x0, y0);
+}
+
 template <int MR, int POST, int PR>
 cudaError_t launch_t(const float* in, void* out, int64_t B, int H, int W, bool partial, bool out16, uint32_t* status,
                      const TailParams& p, cudaStream_t s) {
-  constexpr int kTX = kMW - 2 * PR, kTY = kMH - 2 * PR;
-  const dim3 grid((W + kTX - 1) / kTX, (H + kTY - 1) / kTY, (unsigned)B);
+  using G = TileGeo<MR, PR>;
+  const int tx = (W + G::TX - 1) / G::TX, ty = (H + G::TY - 1) / G::TY;
+  const int64_t ntiles = (int64_t)tx * ty * B;
+  if constexpr (!G::kDB) {
+    const dim3 grid(tx, ty, (unsigned)B);
+    note_launch();
+    if (partial)
+      out16 ? blur_tail_tile_kernel<MR, POST, PR, true, true><<<grid, kThreads, 0, s>>>(in, out, H, W, status, p)
+            : blur_tail_tile_kernel<MR, POST, PR, true, false><<<grid, kThreads, 0, s>>>(in, out, H, W, status, p);
+    else
+      out16 ? blur_tail_tile_kernel<MR, POST, PR, false, true><<<grid, kThreads, 0, s>>>(in, out, H, W, status, p)
+            : blur_tail_tile_kernel<MR, POST, PR, false, false><<<grid, kThreads, 0, s>>>(in, out, H, W, status, p);
+    return cudaGetLastError();
+  }
+  auto k = partial ? (out16 ? blur_tail_kernel<MR, POST, PR, true, true> : blur_tail_kernel<MR, POST, PR, true, false>)
+                   : (out16 ? blur_tail_kernel<MR, POST, PR, false, true> : blur_tail_kernel<MR, POST, PR, false, false>);
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::kSmem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kThreads, G::kSmem);
+  if (e != cudaSuccess) return e;
+  const int64_t grid = std::min<int64_t>(ntiles, (int64_t)std::max(per, 1) * sms);
   note_launch();
-  if (partial)
-    out16 ? blur_tail_kernel<MR, POST, PR, true, true><<<grid, kThreads, 0, s>>>(in, out, H, W, status, p)
-          : blur_tail_kernel<MR, POST, PR, true, false><<<grid, kThreads, 0, s>>>(in, out, H, W, status, p);
-  else
-    out16 ? blur_tail_kernel<MR, POST, PR, false, true><<<grid, kThreads, 0, s>>>(in, out, H, W, status, p)
-          : blur_tail_kernel<MR, POST, PR, false, false><<<grid, kThreads, 0, s>>>(in, out, H, W, status, p);
+  k<<<(unsigned)grid, kThreads, G::kSmem, s>>>(in, out, H, W, status, p, tx, ty, ntiles);
   return cudaGetLastError();
 }
 

@@ -22,6 +22,7 @@
 
 #include "dfc_common.cuh"
 #include "lane_ops.cuh"
+#include "tmem.cuh"
 
 namespace dfc {
 namespace {
@@ -120,9 +121,15 @@ __device__ __forceinline__ void cross3_block(F4 carry[2], const F4 in4[kB], F4 o
   carry[1] = in4[3];
 }
 
+// Carried rows live in tensor memory (tmem.cuh): near-bin box rows nc (6)
+// at TMEM columns 0..23, the cross3 carries m1 m2 m3 f1 f2 (2 rows each) at
+// 24..63; fd (the far bin's one-row delay) and the prefetched rows stay in
+// registers.  184 registers (2 CTAs / SM) became <= 128 (4 CTAs / SM).
+constexpr int kTmNc = 0, kTmM1 = 24, kTmM2 = 32, kTmM3 = 40, kTmF1 = 48, kTmF2 = 56, kMsTmCols = 128;
 struct MsState {
-  F4 nc[6], m1[2], m2[2], m3[2], f1[2], f2[2], fd, nx[kB];
+  F4 fd, nx[kB];
   unsigned um;
+  uint32_t tm;  // this thread's TMEM lane, column 0
 };
 
 // one 4-row block: input rows t0..t0+3 in, output rows t0-3..t0 out.  EDGE:
@@ -155,24 +162,42 @@ __device__ __forceinline__ void ms_block(MsState& S, const float* __restrict__ s
   // near: FULL7 box (rows t0-3+j)
   F4 nb[kB];
   {
-    const F4 col[kB + 6] = {S.nc[0], S.nc[1], S.nc[2], S.nc[3], S.nc[4], S.nc[5], nv[0], nv[1], nv[2], nv[3]};
+    F4 nc[6];
+    tm_wait_st();  // the previous block's carry stores
+    tm_ld_rows(S.tm + kTmNc, nc, 6);
+    const F4 col[kB + 6] = {nc[0], nc[1], nc[2], nc[3], nc[4], nc[5], nv[0], nv[1], nv[2], nv[3]};
     F4 vv[kB];
     vwin3<OpMax>(col, vv);
 #pragma unroll
     for (int j = 0; j < kB; ++j) nb[j] = hwin3<OpMax>(ext_row<3>(vv[j]));
-    S.nc[0] = S.nc[4], S.nc[1] = S.nc[5];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) S.nc[i + 2] = nv[i];
+    const F4 n6[6] = {nc[4], nc[5], nv[0], nv[1], nv[2], nv[3]};
+    tm_st_rows(S.tm + kTmNc, n6, 6);
   }
   // medium: DIAMOND7 = cross3^3 (rows t0-1+j, t0-2+j, t0-3+j)
   F4 a1[kB], a2[kB], a3[kB];
-  cross3_block<EDGE, WOOB>(S.m1, mv, a1, t0 - 1, H, oob);
-  cross3_block<EDGE, WOOB>(S.m2, a1, a2, t0 - 2, H, oob);
-  cross3_block<EDGE, WOOB>(S.m3, a2, a3, t0 - 3, H, oob);
+  {
+    F4 c[2];
+    tm_ld_rows(S.tm + kTmM1, c, 2);
+    cross3_block<EDGE, WOOB>(c, mv, a1, t0 - 1, H, oob);
+    tm_st_rows(S.tm + kTmM1, c, 2);
+    tm_ld_rows(S.tm + kTmM2, c, 2);
+    cross3_block<EDGE, WOOB>(c, a1, a2, t0 - 2, H, oob);
+    tm_st_rows(S.tm + kTmM2, c, 2);
+    tm_ld_rows(S.tm + kTmM3, c, 2);
+    cross3_block<EDGE, WOOB>(c, a2, a3, t0 - 3, H, oob);
+    tm_st_rows(S.tm + kTmM3, c, 2);
+  }
   // far: DIAMOND5 = cross3^2 (rows t0-2+j), delayed one row
   F4 b1[kB], b2[kB];
-  cross3_block<EDGE, WOOB>(S.f1, fv, b1, t0 - 1, H, oob);
-  cross3_block<EDGE, WOOB>(S.f2, b1, b2, t0 - 2, H, oob);
+  {
+    F4 c[2];
+    tm_ld_rows(S.tm + kTmF1, c, 2);
+    cross3_block<EDGE, WOOB>(c, fv, b1, t0 - 1, H, oob);
+    tm_st_rows(S.tm + kTmF1, c, 2);
+    tm_ld_rows(S.tm + kTmF2, c, 2);
+    cross3_block<EDGE, WOOB>(c, b1, b2, t0 - 2, H, oob);
+    tm_st_rows(S.tm + kTmF2, c, 2);
+  }
   const F4 fr[kB] = {S.fd, b2[0], b2[1], b2[2]};
   S.fd = b2[3];
 #pragma unroll
@@ -198,12 +223,9 @@ __device__ __forceinline__ void ms_rows(MsState& S, const float* src, float* dst
 }
 
 template <int VEC>
-__global__ void __launch_bounds__(kMsWarps * 32) ms_fast_kernel(const float* __restrict__ in, float* __restrict__ out,
-                                                                int H, int W, unsigned* __restrict__ umax,
-                                                                const __grid_constant__ MsFastParams p) {
-  const int lane = threadIdx.x & 31;
-  const int S0 = (blockIdx.x * kMsWarps + (threadIdx.x >> 5)) * kMsOwn;
-  if (S0 >= W) return;  // whole warp
+__device__ __forceinline__ void ms_warp(const float* __restrict__ in, float* __restrict__ out, int H, int W,
+                                        unsigned* __restrict__ umax, const MsFastParams& p, int S0, int lane,
+                                        uint32_t tm) {
   const int64_t b = blockIdx.y;
   const float* src = in + b * (int64_t)H * W;
   float* dst = out + b * (int64_t)H * W;
@@ -216,11 +238,18 @@ __global__ void __launch_bounds__(kMsWarps * 32) ms_fast_kernel(const float* __r
     own |= (unsigned)(lane >= 1 && lane <= 30 && x < W) << c;
   }
   MsState S;
+  S.tm = tm;
+  {
+    F4 z[6];
 #pragma unroll
-  for (int i = 0; i < 6; ++i) set_row(S.nc[i], 0.f);
-#pragma unroll
-  for (int i = 0; i < 2; ++i)
-    set_row(S.m1[i], 0.f), set_row(S.m2[i], 0.f), set_row(S.m3[i], 0.f), set_row(S.f1[i], 0.f), set_row(S.f2[i], 0.f);
+    for (int i = 0; i < 6; ++i) set_row(z[i], 0.f);
+    tm_st_rows(tm + kTmNc, z, 6);
+    tm_st_rows(tm + kTmM1, z, 2);
+    tm_st_rows(tm + kTmM2, z, 2);
+    tm_st_rows(tm + kTmM3, z, 2);
+    tm_st_rows(tm + kTmF1, z, 2);
+    tm_st_rows(tm + kTmF2, z, 2);
+  }
   set_row(S.fd, 0.f);
   S.um = 0;
 #pragma unroll
@@ -237,6 +266,29 @@ __global__ void __launch_bounds__(kMsWarps * 32) ms_fast_kernel(const float* __r
   const unsigned um = __reduce_max_sync(kFull, S.um);
   if (lane == 0) atomicMax(umax + b, um);
 }
+
+template <int VEC>
+__global__ void __launch_bounds__(kMsWarps * 32, 4) ms_fast_kernel(const float* __restrict__ in,
+                                                                   float* __restrict__ out, int H, int W,
+                                                                   unsigned* __restrict__ umax,
+                                                                   const __grid_constant__ MsFastParams p) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  static_assert(kMsWarps == 4, "one warp per TMEM lane quarter");
+  __shared__ uint32_t s_tm;
+  if (warp == 0) tm_alloc((uint32_t)__cvta_generic_to_shared(&s_tm), kMsTmCols);
+  tm_fence_before();
+  __syncthreads();
+  tm_fence_after();
+  const uint32_t tmbase = s_tm;
+  const int S0 = (blockIdx.x * kMsWarps + warp) * kMsOwn;
+  if (S0 < W) ms_warp<VEC>(in, out, H, W, umax, p, S0, lane, tmbase + ((uint32_t)(warp * 32) << 16));
+  tm_wait_st();
+  tm_fence_before();
+  __syncthreads();
+  tm_fence_after();
+  if (warp == 0) tm_dealloc(tmbase, kMsTmCols);
+}
+
 
 }  // namespace
 

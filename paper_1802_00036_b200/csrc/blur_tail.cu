@@ -177,7 +177,18 @@ __device__ __forceinline__ void tile_process(const float* __restrict__ sIn, floa
     const int gy = y0 + oy, gx = x0 + ox;
     if (gy >= H || gx >= W) continue;
     const float* m = sM + oy * MW + ox;  // window top-left of the first output (radius PR)
-    const float2 c = make_float2(m[PR * MW + PR], m[PR * MW + PR + 1]);
+    // the pair's window rows: columns ox .. ox + 2 PR + 1 as PR + 1 aligned
+    // 8-byte loads per row (ox even), taps then come from registers
+    float seg[2 * PR + 1][2 * PR + 2];
+#pragma unroll
+    for (int dy = 0; dy <= 2 * PR; ++dy)
+#pragma unroll
+      for (int q = 0; q <= PR; ++q) {
+        const float2 v = *reinterpret_cast<const float2*>(m + dy * MW + 2 * q);
+        seg[dy][2 * q] = v.x;
+        seg[dy][2 * q + 1] = v.y;
+      }
+    const float2 c = make_float2(seg[PR][PR], seg[PR][PR + 1]);
     float2 r = c;
     if constexpr (POST == kPostGauss) {
       // centre-relative: constant neighbourhoods come out exactly constant
@@ -186,7 +197,7 @@ __device__ __forceinline__ void tile_process(const float* __restrict__ sIn, floa
       for (int dy = 0; dy <= 2 * PR; ++dy)
 #pragma unroll
         for (int dx = 0; dx <= 2 * PR; ++dx) {
-          const float2 d = __fadd2_rn(make_float2(m[dy * MW + dx], m[dy * MW + dx + 1]), make_float2(-c.x, -c.y));
+          const float2 d = __fadd2_rn(make_float2(seg[dy][dx], seg[dy][dx + 1]), make_float2(-c.x, -c.y));
           const float w = p.w2[dy * (2 * PR + 1) + dx];
           a = __ffma2_rn(make_float2(w, w), d, a);
         }
@@ -199,7 +210,7 @@ __device__ __forceinline__ void tile_process(const float* __restrict__ sIn, floa
 #pragma unroll
         for (int dx = 0; dx <= 2 * PR; ++dx) {
           if (dy == PR && dx == PR) continue;
-          const float2 d = __fadd2_rn(make_float2(m[dy * MW + dx], m[dy * MW + dx + 1]), make_float2(-c.x, -c.y));
+          const float2 d = __fadd2_rn(make_float2(seg[dy][dx], seg[dy][dx + 1]), make_float2(-c.x, -c.y));
           const float ks = p.ks[dy * (2 * PR + 1) + dx];
           const float2 e = __ffma2_rn(__fmul2_rn(make_float2(p.kv, p.kv), d), d, make_float2(ks, ks));
           const float2 w = make_float2(ex2_ftz(e.x), ex2_ftz(e.y));  // exponents <= 0
@@ -280,8 +291,8 @@ __global__ void __launch_bounds__(kThreads) blur_tail_tile_kernel(const float* _
                                                                   uint32_t* __restrict__ status,
                                                                   const __grid_constant__ TailParams p) {
   using G = TileGeo<MR, PR>;
-  __shared__ float sIn[G::IH * G::IWS];
-  __shared__ float sM[kMH * kMW];
+  __shared__ __align__(16) float sIn[G::IH * G::IWS];
+  __shared__ __align__(16) float sM[kMH * kMW];
   const int64_t b = blockIdx.z;
   const int x0 = blockIdx.x * G::TX, y0 = blockIdx.y * G::TY;
   const float* src = in + b * (int64_t)H * W;

@@ -113,6 +113,27 @@ __device__ __forceinline__ void stage_tile(const float* __restrict__ in, int H, 
   const int x0 = bxi * G::TX, y0 = byi * G::TY;
   const float* src = in + b * (int64_t)H * W;
   const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(sIn);
+  if (x0 - G::HI >= 0 && y0 - G::HI >= 0 && x0 - G::HI + G::IW <= W && y0 - G::HI + G::IH <= H) {
+    // interior tile: no clamping; each thread's (row, column) advances by a
+    // fixed step, so the addresses are updated incrementally
+    constexpr int DY = kThreads / G::IW, DX = kThreads % G::IW;
+    int iy = threadIdx.x / G::IW, ix = threadIdx.x - iy * G::IW;
+    const float* g = src + (int64_t)(y0 - G::HI + iy) * W + (x0 - G::HI + ix);
+    uint32_t d = s0 + 4 * (iy * G::IWS + ix);
+    const int64_t stepA = (int64_t)DY * W + DX, stepB = W - G::IW;
+    for (int i = threadIdx.x; i < G::IH * G::IW; i += kThreads) {
+      cp_async4(d, g);
+      ix += DX;
+      g += stepA;
+      d += 4 * (DY * G::IWS + DX);
+      if (ix >= G::IW) {
+        ix -= G::IW;
+        g += stepB;
+        d += 4 * (G::IWS - G::IW);
+      }
+    }
+    return;
+  }
   for (int i = threadIdx.x; i < G::IH * G::IW; i += kThreads) {
     const int iy = i / G::IW, ix = i - iy * G::IW;
     const float* g = src + (int64_t)clampi(y0 - G::HI + iy, H) * W + clampi(x0 - G::HI + ix, W);

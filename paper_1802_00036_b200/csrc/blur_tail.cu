@@ -160,13 +160,16 @@ __device__ __forceinline__ void tile_process(const float* __restrict__ sIn, floa
     float med[kMedBlockH][kMedBlockW];
     median5_block(sIn + my * IWS + mx, IWS, med);
 #pragma unroll
-    for (int j = 0; j < kMedBlockH; ++j)
+    for (int j = 0; j < kMedBlockH; ++j) {
 #pragma unroll
-      for (int c = 0; c < kMedBlockW; ++c) {
-        float v = med[j][c];
-        if (PARTIAL && !(sIn[(my + j + MR) * IWS + mx + c + MR] > kValid)) v = 0.0f;
-        sM[(my + j) * MW + mx + c] = v;
-      }
+      for (int c = 0; c < kMedBlockW; ++c)
+        if (PARTIAL && !(sIn[(my + j + MR) * IWS + mx + c + MR] > kValid)) med[j][c] = 0.0f;
+      // 16-byte stores (the block's row is 32-byte aligned): 4x fewer shared wavefronts than scalar stores
+#pragma unroll
+      for (int c = 0; c < kMedBlockW; c += 4)
+        *reinterpret_cast<float4*>(sM + (my + j) * MW + mx + c) =
+            make_float4(med[j][c], med[j][c + 1], med[j][c + 2], med[j][c + 3]);
+    }
     if (x0 - PR < 0 || y0 - PR < 0 || x0 - PR + MW > W || y0 - PR + MH > H) {  // tile at a frame edge
       __syncthreads();
       for (int i = threadIdx.x; i < MH * MW; i += kThreads) {

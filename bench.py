@@ -453,7 +453,7 @@ def run_ours(args):
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk, "unit": "GB/s",
             "frac": round(achieved / pk, 4), "traffic": traffic, "peak_source": pk_src,
             "algorithmic_bytes_per_launch": alg_bytes, "kernel_ms_per_launch": round(kern_ms, 4),
-            "kernel": "dfc_fill_batch (fused pipeline kernel + status memsets), CUDA events on its stream"}
+            "kernel": "dfc_fill_batch: every kernel of the step (r0 prologue, [multiscale stage 2], fused pipeline kernel, [blur tail], status finalize), CUDA events on its stream"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -669,12 +669,15 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
     for (int j = 0; j < kB; ++j) {
       a[j] = lds4_t<TIn>(S.stg + j * 512);
       if constexpr (!PRE) {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const float v = a[j].v[c];
-          S.umax = max(S.umax, __float_as_uint(v));
-          a[j].v[c] = v > kValid ? p.md - v : 0.0f;
-        }
+        // invert (depth_core.py:150-156): md - v for a column pair per FFMA2 (exact: -1 * v + md)
+        S.umax = max(max(S.umax, __float_as_uint(a[j].v[0])), __float_as_uint(a[j].v[1]));
+        S.umax = max(max(S.umax, __float_as_uint(a[j].v[2])), __float_as_uint(a[j].v[3]));
+        const float2 d01 = __ffma2_rn(make_float2(a[j].v[0], a[j].v[1]), make_float2(-1.f, -1.f), make_float2(p.md, p.md));
+        const float2 d23 = __ffma2_rn(make_float2(a[j].v[2], a[j].v[3]), make_float2(-1.f, -1.f), make_float2(p.md, p.md));
+        a[j].v[0] = a[j].v[0] > kValid ? d01.x : 0.0f;
+        a[j].v[1] = a[j].v[1] > kValid ? d01.y : 0.0f;
+        a[j].v[2] = a[j].v[2] > kValid ? d23.x : 0.0f;
+        a[j].v[3] = a[j].v[3] > kValid ? d23.y : 0.0f;
       }
     }
     // stage the next block; stops once its stage-5 rows lie above every r0.

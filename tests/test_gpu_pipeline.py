@@ -180,11 +180,12 @@ def test_determinism_across_batch_sizes(P):
     assert np.array_equal(_bits(a), _bits(b)) and np.array_equal(_bits(a), _bits(c))
 
 
-@pytest.mark.parametrize("blur,fill", [("gaussian", "full"), ("bilateral", "partial")])
+@pytest.mark.parametrize("blur,fill", [("gaussian", "full"), ("bilateral", "partial"), ("median_bilateral", "full")])
 def test_many_items_per_cta(P, blur, fill):
     """More frames than SMs: each persistent CTA takes several items in a row, so
     the tensor-memory carry rows, the mbarrier phases and the shared ring carry
-    on across items (and the raw mode runs several fused -> blur-tail rounds).
+    on across items (and the raw mode runs several fused -> blur-tail rounds,
+    the median blur tail's persistent CTAs several double-buffered tiles).
     The big batch must equal the same frames run in chunks small enough for one
     item per CTA, bit for bit, and late frames must match the oracle."""
     n = 320

@@ -1,4 +1,5 @@
-# quick GPU check: the GPU test suite, then config-1 bench lines
+# Quick GPU check (run under gpurun): the GPU test suite, config-1 bench
+# lines, QUICK_CONFIGS="0 2 ..." extra configs, and a launch list of config 1.
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc $?" >> gpurun_out/pytest_gpu.log
 for rep in 1 2; do

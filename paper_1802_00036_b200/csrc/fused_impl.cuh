@@ -319,17 +319,18 @@ __device__ __forceinline__ void row_bits(const F4& v, float md, int i, uint32_t 
   }
 }
 
-// bit i of w[c]: (inverted) validity of row y0 + i (0 outside the frame);
-// PRE: the frame is the stage-2 map in the inverted encoding already
-template <int VEC, bool PRE, typename T>
+// bit i of w[c] (i < N = 16 or 32): (inverted) validity of row y0 + i (0
+// outside the frame); PRE: the frame is the stage-2 map in the inverted encoding already
+template <int VEC, bool PRE, int N, typename T>
 __device__ __forceinline__ void load_bits(const LaneCols<VEC, T>& lc, int H, int W, int y0, float md, uint32_t w[4],
                                           unsigned& umax) {
+  static_assert(N == 16 || N == 32, "16-row groups");
 #pragma unroll
   for (int c = 0; c < 4; ++c) w[c] = 0;
   if (y0 >= H) return;
-  if (y0 >= 0 && y0 + 32 <= H) {
+  if (y0 >= 0 && y0 + N <= H) {
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < N / 16; ++h) {
       F4 v[16];
       const int64_t off = (int64_t)(y0 + 16 * h) * W;
 #pragma unroll
@@ -338,9 +339,9 @@ __device__ __forceinline__ void load_bits(const LaneCols<VEC, T>& lc, int H, int
       for (int i = 0; i < 16; ++i) row_bits<PRE>(v[i], md, 16 * h + i, w, umax);
     }
   } else {
-    const uint32_t rows = (uint32_t)(((1ull << (min(H - y0, 32))) - 1) & ~((1ull << min(max(-y0, 0), 32)) - 1));
+    const uint32_t rows = (uint32_t)(((1ull << (min(H - y0, N))) - 1) & ~((1ull << min(max(-y0, 0), N)) - 1));
 #pragma unroll 4
-    for (int i = 0; i < 32; ++i) {
+    for (int i = 0; i < N; ++i) {
       const int y = min(max(y0 + i, 0), H - 1);
       row_bits<PRE>(lc.row((int64_t)y * W), md, i, w, umax);
     }
@@ -387,8 +388,11 @@ __device__ __forceinline__ void phase1(const T* frame, const Params& p, int x0, 
   const int H = p.H, W = p.W;
   uint32_t prv[4] = {0, 0, 0, 0}, cur[4], nxt[4];
   const LaneCols<VEC, T> lc(frame, x0, W);
-  load_bits<VEC, PRE>(lc, H, W, s0, p.md, cur, umax);
-  load_bits<VEC, PRE>(lc, H, W, s0 + 32, p.md, nxt, umax);
+  // the window of block b is rows [s0+32b-16, s0+32b+48): nxt holds only the
+  // 16 rows below the block (a block usually finds every r0; the rest of the
+  // next block is read only when it is needed)
+  load_bits<VEC, PRE, 32>(lc, H, W, s0, p.md, cur, umax);
+  load_bits<VEC, PRE, 16>(lc, H, W, s0 + 32, p.md, nxt, umax);
   int r0[4] = {-1, -1, -1, -1};
   uint64_t cm[4];
 #pragma unroll
@@ -430,12 +434,14 @@ __device__ __forceinline__ void phase1(const T* frame, const Params& p, int x0, 
       done = done && (r0[c] >= 0 || !(incol >> c & 1));
     }
     if (__all_sync(kFull, done || !needed)) break;
+    uint32_t nhi[4];
+    load_bits<VEC, PRE, 16>(lc, H, W, s0 + 32 * b + 48, p.md, nhi, umax);
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       prv[c] = cur[c];
-      cur[c] = nxt[c];
+      cur[c] = nxt[c] | nhi[c] << 16;
     }
-    load_bits<VEC, PRE>(lc, H, W, s0 + 32 * (b + 2), p.md, nxt, umax);
+    load_bits<VEC, PRE, 16>(lc, H, W, s0 + 32 * (b + 2), p.md, nxt, umax);
   }
 #pragma unroll
   for (int c = 0; c < 4; ++c) T0[c] = r0[c] >= 0 ? (H - 1 - r0[c]) : INT_MAX;

@@ -141,6 +141,13 @@ int dfc_fill_batch(const float* in, float* out, int64_t B, int32_t H, int32_t W,
 int dfc_fill_finish(const float* in, float* out, int64_t B, int32_t H, int32_t W, const dfc_config* cfg,
                     uint32_t* frame_status, int32_t* large_fill_iters, void* workspace, size_t ws_bytes,
                     void* stream);
+/* RunStats' density counters (pipeline.py:138-141, 192-202) of the last
+ * dfc_fill_batch (+ dfc_fill_finish) run with this workspace, config and shape:
+ * valid_counts[B][2] (device, uint32) = pixels > 0.1 in the input and in the
+ * output of each frame.  They are counted inside the fused read / store
+ * passes (density = count / (H * W)); enqueued on `stream` (no sync). */
+int dfc_fill_counts(const dfc_config* cfg, int64_t B, int32_t H, int32_t W, const void* workspace, size_t ws_bytes,
+                    uint32_t* valid_counts, void* stream);
 
 /* ---- operator surface (_native_ops / _numpy_ops), batched --------------- */
 /* Workspace for the separable ops (box max/min, gaussian): B*H*W*8 bytes. */

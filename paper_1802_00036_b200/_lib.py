@@ -39,7 +39,7 @@ FILL_CODES = {"full": 0, "partial": 1}
 # every symbol include/dfc.h declares
 EXPORTS = (
     "dfc_abi_version", "dfc_last_error_string", "dfc_kernel_launches", "dfc_config_init", "dfc_workspace_bytes",
-    "dfc_fill_batch", "dfc_fill_finish", "dfc_op_workspace_bytes", "dfc_box_max", "dfc_box_min",
+    "dfc_fill_batch", "dfc_fill_finish", "dfc_fill_counts", "dfc_op_workspace_bytes", "dfc_box_max", "dfc_box_min",
     "dfc_offsets_max", "dfc_offsets_min", "dfc_median", "dfc_gaussian_separable", "dfc_bilateral",
     "dfc_invert", "dfc_validate", "dfc_masked_fill", "dfc_extend_to_top", "dfc_count_empty",
     "dfc_reimpose", "dfc_workspace_bytes_raw16", "dfc_fill_batch_raw16", "dfc_decode_raw16", "dfc_encode_raw16",
@@ -114,6 +114,7 @@ def load(require: bool = True):
         "dfc_workspace_bytes": (sz, [cfgp, i64, i32, i32]),
         "dfc_fill_batch": (ctypes.c_int, [vp, vp, i64, i32, i32, cfgp, u32p, vp, vp, sz, vp]),
         "dfc_fill_finish": (ctypes.c_int, [vp, vp, i64, i32, i32, cfgp, u32p, vp, vp, sz, vp]),
+        "dfc_fill_counts": (ctypes.c_int, [cfgp, i64, i32, i32, vp, sz, vp, vp]),
         "dfc_op_workspace_bytes": (sz, [i64, i32, i32]),
         "dfc_box_max": (ctypes.c_int, [vp, vp, i64, i32, i32, i32, vp, sz, vp]),
         "dfc_box_min": (ctypes.c_int, [vp, vp, i64, i32, i32, i32, vp, sz, vp]),

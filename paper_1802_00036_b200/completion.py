@@ -263,7 +263,8 @@ def complete_with_stats(sparse, config: PipelineConfig | None = None) -> tuple[D
         raise EncodingError("pipeline input must be direct-encoded")
     dev = _device()
     x = torch.from_numpy(np.array(sparse.values, dtype=np.float32, copy=True)).to(dev)
-    n_valid = int(np.count_nonzero(sparse.values > np.float32(domain.VALIDITY_THRESHOLD)))
+    # input density: the device validity reduction (pipeline.py:138-141)
+    n_valid = int(ops.validate(x)[1].cpu()[0])
     if n_valid == 0:
         raise DegenerateInputError("input depth map has no valid pixels")
     config = fit_to_frame(config, sparse.height, sparse.width)
@@ -300,12 +301,14 @@ def complete_with_stats(sparse, config: PipelineConfig | None = None) -> tuple[D
     times = [ev[i].elapsed_time(ev[i + 1]) for i in range(len(STAGE_NAMES))]
     if not full:
         times[4] = times[5] = 0.0
+    # output density: the device count of pixels > 0.1 (pipeline.py:192-202)
+    n_out = dense.numel() - int(ops.count_empty(dense)[0].cpu())
     out = dense.cpu().numpy()
     stats = RunStats(
         stage_ms=tuple(zip(STAGE_NAMES, times)),
         total_ms=ev[0].elapsed_time(ev[-1]),
         input_density=n_valid / sparse.values.size,
-        output_density=float(np.count_nonzero(out > np.float32(domain.VALIDITY_THRESHOLD))) / out.size,
+        output_density=n_out / out.size,
         large_fill_iterations=iters,
     )
     return DepthMap._wrap(out, DepthEncoding.DIRECT), stats

@@ -43,6 +43,7 @@ struct TailParams {
   float w2[25];  // Gaussian 2-D taps w_i * w_j (row-major, radius PR)
   float ks[25];  // bilateral: log2(e) * spatial exponent per tap (dy^2 + dx^2) / (-2 sigma_s^2)
   float kv;      // bilateral: log2(e) / (-2 sigma_v^2)
+  unsigned* vcount;  // [B][2] (may be null): [1] += valid outputs (RunStats.output_density)
 };
 
 #define DFC_CSWAP(a, b)            \
@@ -150,6 +151,7 @@ __device__ __forceinline__ void tile_process(const float* __restrict__ sIn, floa
   constexpr int HI = G::HI, kTX = G::TX, kTY = G::TY, IWS = G::IWS;
   constexpr int MW = kMW, MH = kMH;
   bool over = false;  // OUT16: an output >= 256 m
+  unsigned nvalid = 0;
 
   // stage-7a: median (or copy) on the tile + blur halo, at frame-clamped centres
   if constexpr (MR == 2) {
@@ -250,6 +252,7 @@ __device__ __forceinline__ void tile_process(const float* __restrict__ sIn, floa
       if (PARTIAL && POST != kPostNone && !(cc[h] > kValid)) o[h] = 0.0f;
       o[h] = o[h] > kValid ? p.md - o[h] : 0.0f;
     }
+    nvalid += (o[0] > kValid) + (gx + 1 < W && o[1] > kValid);
     const int64_t off = b * (int64_t)H * W + (int64_t)gy * W + gx;
     if constexpr (OUT16) {
       uint16_t* q = static_cast<uint16_t*>(out_v) + off;
@@ -273,6 +276,10 @@ __device__ __forceinline__ void tile_process(const float* __restrict__ sIn, floa
     }
   }
   if (OUT16 && over) atomicOr(status + b, DFC_ST_ENCODE);  // write_depth_png raises (kitti_io.py:60-61)
+  if (p.vcount) {
+    nvalid = __reduce_add_sync(0xffffffffu, nvalid);
+    if ((threadIdx.x & 31) == 0 && nvalid) atomicAdd(p.vcount + 2 * b + 1, nvalid);
+  }
 }
 
 // With the median: persistent CTAs walk the tiles (frame-major) with two
@@ -335,15 +342,27 @@ cudaError_t launch_t(const float* in, void* out, int64_t B, int H, int W, bool p
   const int tx = (W + G::TX - 1) / G::TX, ty = (H + G::TY - 1) / G::TY;
   const int64_t ntiles = (int64_t)tx * ty * B;
   if constexpr (!G::kDB) {
-    const dim3 grid(tx, ty, (unsigned)B);
-    note_launch();
-    if (partial)
-      out16 ? blur_tail_tile_kernel<MR, POST, PR, true, true><<<grid, kThreads, 0, s>>>(in, out, H, W, status, p)
-            : blur_tail_tile_kernel<MR, POST, PR, true, false><<<grid, kThreads, 0, s>>>(in, out, H, W, status, p);
-    else
-      out16 ? blur_tail_tile_kernel<MR, POST, PR, false, true><<<grid, kThreads, 0, s>>>(in, out, H, W, status, p)
-            : blur_tail_tile_kernel<MR, POST, PR, false, false><<<grid, kThreads, 0, s>>>(in, out, H, W, status, p);
-    return cudaGetLastError();
+    // grid.z holds at most 65535 frames: chunk the batch
+    const int64_t HW = (int64_t)H * W;
+    for (int64_t f0 = 0; f0 < B; f0 += 65535) {
+      const int64_t C = std::min<int64_t>(65535, B - f0);
+      const dim3 grid(tx, ty, (unsigned)C);
+      const float* ic = in + f0 * HW;
+      void* oc = static_cast<char*>(out) + f0 * HW * (out16 ? 2 : 4);
+      uint32_t* sc = status ? status + f0 : nullptr;
+      TailParams pc = p;
+      if (pc.vcount) pc.vcount += 2 * f0;
+      note_launch();
+      if (partial)
+        out16 ? blur_tail_tile_kernel<MR, POST, PR, true, true><<<grid, kThreads, 0, s>>>(ic, oc, H, W, sc, pc)
+              : blur_tail_tile_kernel<MR, POST, PR, true, false><<<grid, kThreads, 0, s>>>(ic, oc, H, W, sc, pc);
+      else
+        out16 ? blur_tail_tile_kernel<MR, POST, PR, false, true><<<grid, kThreads, 0, s>>>(ic, oc, H, W, sc, pc)
+              : blur_tail_tile_kernel<MR, POST, PR, false, false><<<grid, kThreads, 0, s>>>(ic, oc, H, W, sc, pc);
+      const cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
   }
   auto k = partial ? (out16 ? blur_tail_kernel<MR, POST, PR, true, true> : blur_tail_kernel<MR, POST, PR, true, false>)
                    : (out16 ? blur_tail_kernel<MR, POST, PR, false, true> : blur_tail_kernel<MR, POST, PR, false, false>);
@@ -376,7 +395,7 @@ bool blur_tail_supported(const dfc_config& c) {
 
 // Blur stage + invert back for B frames (in: inverted map; out: direct depth).
 cudaError_t launch_blur_tail(const float* in, void* out, int64_t B, int H, int W, const dfc_config& c, bool out_raw,
-                             uint32_t* status, cudaStream_t s) {
+                             uint32_t* status, unsigned* vcount, cudaStream_t s) {
   const int bm = c.blur_mode;
   const bool med = bm == DFC_BLUR_MEDIAN || bm == DFC_BLUR_MEDIAN_BILATERAL || bm == DFC_BLUR_MEDIAN_GAUSSIAN;
   const bool gauss = bm == DFC_BLUR_GAUSSIAN || bm == DFC_BLUR_MEDIAN_GAUSSIAN;
@@ -384,6 +403,7 @@ cudaError_t launch_blur_tail(const float* in, void* out, int64_t B, int H, int W
   const bool partial = c.fill_mode == DFC_FILL_PARTIAL;
   TailParams p{};
   p.md = c.max_depth;
+  p.vcount = vcount;
   int pr = 0;
   if (gauss) {
     pr = c.gaussian_size / 2;

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -97,12 +98,15 @@ struct StagedBufs {
   float *a, *b, *c, *d, *e;  // e follows d: (d,e) doubles as a float64 scratch
   int64_t *n_valid, *counts;
   unsigned long long* total;
+  void* lf;  // large-fill loop scratch (dfc::large_fill_scratch_bytes)
 };
 
+// frames per staged round: about 64 MB of frames (at most 65535: grid.y limits)
 int64_t staged_chunk(int64_t B, int H, int W) {
   const int64_t per = (int64_t)H * W * 4;
   int64_t c = ((int64_t)64 << 20) / per;
   if (c < 1) c = 1;
+  if (c > 65535) c = 65535;
   return c < B ? c : B;
 }
 
@@ -111,7 +115,15 @@ size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 size_t staged_bytes(int64_t chunk, int H, int W) {
   if (chunk <= 0) return 0;
   const size_t f = align256((size_t)chunk * H * W * 4);
-  return 5 * f + align256(chunk * 8) * 2 + 256;
+  return 5 * f + align256(chunk * 8) * 2 + 256 + align256(dfc::large_fill_scratch_bytes(chunk));
+}
+
+// fused-path fallback: frames flagged by the fused kernel are gathered into
+// [in][out] maps of one staged chunk, with their indices, statuses and counts
+size_t fallback_bytes(int64_t chunk, int H, int W) {
+  if (chunk <= 0) return 0;
+  return 2 * align256((size_t)chunk * H * W * 4) + align256(chunk * 8) + 2 * align256(chunk * 4) +
+         align256(chunk * 8);
 }
 
 StagedBufs carve_staged(void* ws, int64_t chunk, int H, int W) {
@@ -126,6 +138,7 @@ StagedBufs carve_staged(void* ws, int64_t chunk, int H, int W) {
   s.n_valid = (int64_t*)(p + 5 * f);
   s.counts = (int64_t*)(p + 5 * f + align256(chunk * 8));
   s.total = (unsigned long long*)(p + 5 * f + 2 * align256(chunk * 8));
+  s.lf = p + 5 * f + 2 * align256(chunk * 8) + 256;
   return s;
 }
 
@@ -154,7 +167,7 @@ int gaussian_weights(int size, double sigma, double* w) {
 }
 
 int run_staged(const float* in, float* out, int64_t B, int H, int W, const dfc_config& c, uint32_t* status,
-               int32_t* iters, void* ws, size_t ws_bytes, cudaStream_t s) {
+               int32_t* iters, unsigned* vcount, void* ws, size_t ws_bytes, cudaStream_t s) {
   const int64_t chunk = staged_chunk(B, H, W);
   if (!ws || ws_bytes < staged_bytes(chunk, H, W)) return fail(DFC_E_WORKSPACE, "workspace too small (staged)");
   const int64_t HW = (int64_t)H * W;
@@ -205,7 +218,12 @@ int run_staged(const float* in, float* out, int64_t B, int H, int W, const dfc_c
       DFC_CK(dfc::launch_extend_to_top(q.a, q.b, C, H, W, s));
       cur = q.b;
       spare = q.a;
-      // 6. large fill, iterated per frame while empties remain
+      // 6. large fill, iterated per frame while empties remain: device-gated
+      //    tiled iterations, one host check per group of iterations
+      if (dfc::large_fill_tiled_supported(c.large_fill_size / 2)) {
+        DFC_CK(dfc::launch_large_fill_loop(cur, spare, C, H, W, c.large_fill_size / 2, c.large_fill_max_iters, it,
+                                           q.lf, s));
+      } else
       for (int k = 0; k < c.large_fill_max_iters; ++k) {
         DFC_CK(cudaMemsetAsync(q.counts, 0, C * 8, s));
         DFC_CK(cudaMemsetAsync(q.total, 0, 8, s));
@@ -221,7 +239,8 @@ int run_staged(const float* in, float* out, int64_t B, int H, int W, const dfc_c
     }
     // 7 + 8. blur stage (pipeline._blur_stage :206-238) and invert back, one tiled kernel
     if (dfc::blur_tail_supported(c)) {
-      DFC_CK(dfc::launch_blur_tail(cur, y, C, H, W, c, false, st, s));
+      DFC_CK(dfc::launch_blur_tail(cur, y, C, H, W, c, false, st, nullptr, s));
+      if (vcount) DFC_CK(dfc::launch_valid_counts(y, HW, C, q.n_valid, vcount + 2 * f0, s));
       continue;
     }
     // exact float64 blurs: one op per launch
@@ -248,13 +267,14 @@ int run_staged(const float* in, float* out, int64_t B, int H, int W, const dfc_c
     }
     // 8. invert back
     DFC_CK(dfc::launch_invert(cur, y, HW, C, c.max_depth, nullptr, s));
+    if (vcount) DFC_CK(dfc::launch_valid_counts(y, HW, C, q.n_valid, vcount + 2 * f0, s));
   }
   return DFC_OK;
 }
 
-// workspace layout: [fused region][staged region]
+// workspace layout: [fused region][staged region][valid counts [B][2] u32]
 struct WsLayout {
-  size_t fused, staged, total;
+  size_t fused, staged, cnt, total;
   int64_t chunk;
   bool use_fused;
 };
@@ -262,15 +282,17 @@ struct WsLayout {
 WsLayout ws_layout(const dfc_config& c, int64_t B, int H, int W) {
   WsLayout L;
   L.use_fused = !(c.flags & DFC_F_FORCE_STAGED) && dfc::fused_supported(c, H, W);
+  L.chunk = staged_chunk(B, H, W);
   if (L.use_fused) {
     L.fused = align256(dfc::fused_workspace_bytes(c, B, H, W));
-    L.chunk = 1;  // fallback frames are re-run one at a time
+    // flagged frames are gathered and finished a staged chunk at a time
+    L.staged = staged_bytes(L.chunk > 0 ? L.chunk : 1, H, W) + fallback_bytes(L.chunk > 0 ? L.chunk : 1, H, W);
   } else {
     L.fused = 0;
-    L.chunk = staged_chunk(B, H, W);
+    L.staged = staged_bytes(L.chunk > 0 ? L.chunk : 1, H, W);
   }
-  L.staged = staged_bytes(L.chunk > 0 ? L.chunk : 1, H, W);
-  L.total = L.fused + L.staged;
+  L.cnt = align256((size_t)B * 8);
+  L.total = L.fused + L.staged + L.cnt;
   return L;
 }
 
@@ -339,11 +361,12 @@ int dfc_fill_batch(const float* in, float* out, int64_t B, int32_t H, int32_t W,
   cudaStream_t s = as_stream(stream);
   DFC_CK(cudaMemsetAsync(frame_status, 0, B * 4, s));
   if (large_fill_iters) DFC_CK(cudaMemsetAsync(large_fill_iters, 0, B * 4, s));
+  unsigned* vcount = reinterpret_cast<unsigned*>(static_cast<char*>(workspace) + L.fused + L.staged);
   if (!L.use_fused) {
-    return run_staged(in, out, B, H, W, c, frame_status, large_fill_iters, static_cast<char*>(workspace) + L.fused,
-                      L.staged, s);
+    return run_staged(in, out, B, H, W, c, frame_status, large_fill_iters, vcount,
+                      static_cast<char*>(workspace) + L.fused, L.staged, s);
   }
-  DFC_CK(dfc::launch_fused(in, out, B, H, W, c, frame_status, large_fill_iters, workspace, L.fused, s));
+  DFC_CK(dfc::launch_fused(in, out, B, H, W, c, frame_status, large_fill_iters, vcount, workspace, L.fused, s));
   if (c.flags & DFC_F_NO_FINISH) return DFC_OK;
   return dfc_fill_finish(in, out, B, H, W, cfg, frame_status, large_fill_iters, workspace, ws_bytes, stream);
 }
@@ -366,17 +389,50 @@ int dfc_fill_finish(const float* in, float* out, int64_t B, int32_t H, int32_t W
   std::vector<uint32_t> st(B);
   DFC_CK(cudaMemcpyAsync(st.data(), frame_status, B * 4, cudaMemcpyDeviceToHost, s));
   DFC_CK(cudaStreamSynchronize(s));
+  std::vector<int64_t> idx;
+  for (int64_t b = 0; b < B; ++b)
+    if (st[b] & 0x200u) idx.push_back(b);  // internal "needs staged" bit set by the fused kernel
+  // the flagged frames, a staged chunk at a time: gather -> staged pipeline
+  // (device-gated large-fill loop) -> scatter outputs, statuses and counts
   const int64_t HW = (int64_t)H * W;
-  for (int64_t b = 0; b < B; ++b) {
-    if (!(st[b] & 0x200u)) continue;  // internal "needs staged" bit set by the fused kernel
-    DFC_CK(cudaMemsetAsync(frame_status + b, 0, 4, s));
-    if (large_fill_iters) DFC_CK(cudaMemsetAsync(large_fill_iters + b, 0, 4, s));
-    int rc = run_staged(in + b * HW, out + b * HW, 1, H, W, c, frame_status + b,
-                        large_fill_iters ? large_fill_iters + b : nullptr, static_cast<char*>(workspace) + L.fused,
-                        L.staged, s);
+  const int64_t chunk = L.chunk;
+  char* sw = static_cast<char*>(workspace) + L.fused;
+  const size_t sb = staged_bytes(chunk, H, W);
+  const size_t f = align256((size_t)chunk * HW * 4);
+  float* g_in = reinterpret_cast<float*>(sw + sb);
+  float* g_out = reinterpret_cast<float*>(sw + sb + f);
+  int64_t* g_idx = reinterpret_cast<int64_t*>(sw + sb + 2 * f);
+  uint32_t* g_st = reinterpret_cast<uint32_t*>(sw + sb + 2 * f + align256(chunk * 8));
+  int32_t* g_it = reinterpret_cast<int32_t*>(sw + sb + 2 * f + align256(chunk * 8) + align256(chunk * 4));
+  unsigned* g_vc = reinterpret_cast<unsigned*>(sw + sb + 2 * f + align256(chunk * 8) + 2 * align256(chunk * 4));
+  unsigned* vcount = reinterpret_cast<unsigned*>(static_cast<char*>(workspace) + L.fused + L.staged);
+  for (size_t i0 = 0; i0 < idx.size(); i0 += (size_t)chunk) {
+    const int64_t C = std::min<int64_t>(chunk, (int64_t)idx.size() - (int64_t)i0);
+    DFC_CK(cudaMemcpyAsync(g_idx, idx.data() + i0, C * 8, cudaMemcpyHostToDevice, s));
+    DFC_CK(dfc::launch_gather_frames(in, g_in, HW, g_idx, C, false, s));
+    DFC_CK(cudaMemsetAsync(g_st, 0, C * 4, s));
+    DFC_CK(cudaMemsetAsync(g_it, 0, C * 4, s));
+    int rc = run_staged(g_in, g_out, C, H, W, c, g_st, g_it, g_vc, sw, sb, s);
     if (rc) return rc;
-    DFC_CK(dfc::launch_or_status(frame_status + b, DFC_ST_FALLBACK, s));
+    DFC_CK(dfc::launch_gather_frames(g_out, out, HW, g_idx, C, true, s));
+    DFC_CK(dfc::launch_scatter_status(g_st, g_it, g_vc, g_idx, C, frame_status, large_fill_iters, vcount,
+                                      DFC_ST_FALLBACK, s));
+    DFC_CK(cudaStreamSynchronize(s));  // idx (host) is reused by the next chunk's copy
   }
+  return DFC_OK;
+}
+
+int dfc_fill_counts(const dfc_config* cfg, int64_t B, int32_t H, int32_t W, const void* workspace, size_t ws_bytes,
+                    uint32_t* valid_counts, void* stream) {
+  if (!cfg) return fail(DFC_E_INVALID, "null config");
+  int rc = check_shape(B, H, W);
+  if (rc) return rc;
+  if (B == 0) return DFC_OK;
+  const dfc_config c = fit_to_frame(*cfg, H, W);
+  const WsLayout L = ws_layout(c, B, H, W);
+  if (!workspace || ws_bytes < L.total || !valid_counts) return fail(DFC_E_INVALID, "bad workspace or counts buffer");
+  DFC_CK(cudaMemcpyAsync(valid_counts, static_cast<const char*>(workspace) + L.fused + L.staged, (size_t)B * 8,
+                         cudaMemcpyDeviceToDevice, as_stream(stream)));
   return DFC_OK;
 }
 
@@ -563,7 +619,8 @@ int dfc_fill_batch_raw16(const uint16_t* raw_in, void* out, int32_t out_raw, int
     float* fout = reinterpret_cast<float*>(ws + L.total + HW4);
     DFC_CK(cudaMemsetAsync(frame_status, 0, B * 4, s));
     if (large_fill_iters) DFC_CK(cudaMemsetAsync(large_fill_iters, 0, B * 4, s));
-    DFC_CK(dfc::launch_fused(raw_in, out, B, H, W, c, frame_status, large_fill_iters, ws, L.fused, s,
+    unsigned* vcount = reinterpret_cast<unsigned*>(ws + L.fused + L.staged);
+    DFC_CK(dfc::launch_fused(raw_in, out, B, H, W, c, frame_status, large_fill_iters, vcount, ws, L.fused, s,
                              out_raw ? 2 : 1));
     if (c.flags & DFC_F_NO_FINISH) return DFC_OK;  // the caller re-runs frames with status bit 0x200
     unsigned long long nfb = 0;
@@ -580,7 +637,7 @@ int dfc_fill_batch_raw16(const uint16_t* raw_in, void* out, int32_t out_raw, int
       DFC_CK(dfc::launch_decode_raw16(raw_in + b * HW, fin, HW, s));
       float* dst = out_raw ? fout : static_cast<float*>(out) + b * HW;
       rc = run_staged(fin, dst, 1, H, W, c, frame_status + b, large_fill_iters ? large_fill_iters + b : nullptr,
-                      ws + L.fused, L.staged, s);
+                      vcount + 2 * b, ws + L.fused, L.staged, s);
       if (rc) return rc;
       if (out_raw) DFC_CK(dfc::launch_encode_raw16(fout, static_cast<uint16_t*>(out) + b * HW, HW, HW, frame_status + b, s));
       DFC_CK(dfc::launch_or_status(frame_status + b, DFC_ST_FALLBACK, s));

@@ -92,23 +92,37 @@ cudaError_t launch_iter_update(const int64_t* counts, int32_t* iters, int64_t B,
                                cudaStream_t s);
 cudaError_t launch_or_status(uint32_t* status, uint32_t bits, cudaStream_t s);
 cudaError_t launch_finalize_status(const int64_t* n_valid, uint32_t* status, int64_t B, cudaStream_t s);
+// large_fill.cu: device-gated multi-iteration large fill, frame gather / scatter
+bool large_fill_tiled_supported(int r);
+size_t large_fill_scratch_bytes(int64_t B);
+cudaError_t launch_large_fill_loop(float* buf0, float* buf1, int64_t B, int H, int W, int r, int max_iters,
+                                   int32_t* iters, void* scratch, cudaStream_t s);
+cudaError_t launch_gather_frames(const float* src, float* dst, int64_t HW, const int64_t* idx, int64_t C, bool scatter,
+                                 cudaStream_t s);
+cudaError_t launch_scatter_status(const uint32_t* st, const int32_t* it, const unsigned* vc, const int64_t* idx,
+                                  int64_t C, uint32_t* status, int32_t* iters, unsigned* vcount, uint32_t bits,
+                                  cudaStream_t s);
+cudaError_t launch_valid_counts(const float* out, int64_t HW, int64_t C, const int64_t* n_valid, unsigned* vcount,
+                                cudaStream_t s);
 
 // ---- blur stage + invert back in one tiled kernel (blur_tail.cu) ---------
 bool blur_tail_supported(const dfc_config& c);
 cudaError_t launch_blur_tail(const float* in, void* out, int64_t B, int H, int W, const dfc_config& c, bool out_raw,
-                             uint32_t* status, cudaStream_t s);
+                             uint32_t* status, unsigned* vcount, cudaStream_t s);
 
 // ---- multiscale stage 1 + 2 (multiscale.cu) -------------------------------
 bool multiscale_stage2_supported(const dfc_config& c);
 cudaError_t launch_multiscale_stage2(const float* in, float* out, int64_t B, int H, int W, const dfc_config& c,
-                                     const int32_t* const offs[3], const int n[3], unsigned* umax, cudaStream_t s);
+                                     const int32_t* const offs[3], const int n[3], unsigned* umax, unsigned* vcount,
+                                     cudaStream_t s);
 
 // ---- fused pipeline (fused.cu) -------------------------------------------
 struct FusedPlan;
 bool fused_supported(const dfc_config& c, int H, int W);
 size_t fused_workspace_bytes(const dfc_config& c, int64_t B, int H, int W);
 cudaError_t launch_fused(const void* in, void* out, int64_t B, int H, int W, const dfc_config& c,
-                         uint32_t* status, int32_t* iters, void* ws, size_t ws_bytes, cudaStream_t s, int io = 0);
+                         uint32_t* status, int32_t* iters, unsigned* vcount, void* ws, size_t ws_bytes,
+                         cudaStream_t s, int io = 0);
 bool fused_supports_raw16(const dfc_config& c, int H, int W);
 
 }  // namespace dfc

@@ -17,22 +17,42 @@ namespace {
 
 // Per-frame status from the input's largest bit pattern; frames whose max is
 // suspicious (negative sign, non-finite, >= max_depth) are rescanned.
-__global__ void finalize_kernel(const float* __restrict__ in, int64_t HW, const unsigned* __restrict__ umax,
-                                uint32_t* status, float md, bool in_raw) {
+// vcount[2b] holds the inverted-valid inputs the fused kernel read (every
+// pixel once); an input can be valid (> 0.1) but inverted-invalid only when
+// md - v <= 0.1, i.e. only if the frame's max already is (md - v is monotone),
+// so only such frames (count_in) are recounted here with the plain v > 0.1
+// (pipeline.py:138-141), the raw input as raw > 25 (raw / 256 > 0.1).
+__global__ void finalize_kernel(const void* __restrict__ in_v, int64_t HW, const unsigned* __restrict__ umax,
+                                uint32_t* status, float md, bool in_raw, unsigned* vcount, bool count_in) {
   const int64_t b = blockIdx.x;
   const unsigned u = umax[b];
+  const float uf = __uint_as_float(u);
+  const bool rare = count_in && uf > kValid && uf < md && !(__fadd_rn(md, -uf) > kValid);
   if (in_raw) {  // raw / 256 is finite and >= 0: the max decides RANGE and DEGENERATE alone
     if (threadIdx.x == 0 && u >= __float_as_uint(md)) atomicOr(status + b, DFC_ST_RANGE);
     if (threadIdx.x == 0 && u <= __float_as_uint(kValid)) atomicOr(status + b, DFC_ST_DEGENERATE);
-    return;
-  }
-  if (u < __float_as_uint(md)) {
+    if (!rare) return;
+  } else if (u < __float_as_uint(md) && !rare) {
     if (u <= __float_as_uint(kValid) && threadIdx.x == 0) atomicOr(status + b, DFC_ST_DEGENERATE);
     return;
   }
+  __shared__ unsigned sb, sv, sn;
+  if (threadIdx.x == 0) sb = 0, sv = 0, sn = 0;
+  __syncthreads();
+  if (in_raw) {  // rare only: recount (raw / 256 > 0.1 <=> raw > 25)
+    const uint16_t* src = static_cast<const uint16_t*>(in_v) + b * HW;
+    unsigned n = 0;
+    for (int64_t i = threadIdx.x; i < HW; i += blockDim.x) n += src[i] > 25u;
+    n = __reduce_add_sync(kFull, n);
+    if ((threadIdx.x & 31) == 0 && n) atomicAdd(&sn, n);
+    __syncthreads();
+    if (threadIdx.x == 0) vcount[2 * b] = sn;
+    return;
+  }
+  const float* in = static_cast<const float*>(in_v);
   const float* src = in + b * HW;
   uint32_t bits = 0;
-  bool anyv = false;
+  unsigned n = 0;
   for (int64_t i = threadIdx.x; i < HW; i += blockDim.x) {
     const float v = src[i];
     if (!isfinite(v))
@@ -41,22 +61,20 @@ __global__ void finalize_kernel(const float* __restrict__ in, int64_t HW, const 
       bits |= DFC_ST_NEGATIVE;
     else if (v >= md)
       bits |= DFC_ST_RANGE;
-    anyv |= v > kValid;
+    n += v > kValid;
   }
   bits = __reduce_or_sync(kFull, bits);
-  anyv = __any_sync(kFull, anyv);
-  __shared__ unsigned sb, sv;
-  if (threadIdx.x == 0) sb = 0, sv = 0;
-  __syncthreads();
+  n = __reduce_add_sync(kFull, n);
   if ((threadIdx.x & 31) == 0) {
     atomicOr(&sb, bits);
-    if (anyv) atomicOr(&sv, 1u);
+    if (n) atomicOr(&sv, 1u), atomicAdd(&sn, n);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     uint32_t st = sb;
     if (!sv) st |= DFC_ST_DEGENERATE;
     if (st) atomicOr(status + b, st);
+    if (count_in) vcount[2 * b] = sn;
   }
 }
 
@@ -169,7 +187,8 @@ bool fused_supports_raw16(const dfc_config& c, int H, int W) {
 
 // io 0: float32 in / out; 1: 16-bit KITTI raw in, float32 out; 2: raw in / raw out
 cudaError_t launch_fused(const void* in_v, void* out_v, int64_t B, int H, int W, const dfc_config& c,
-                         uint32_t* status, int32_t* iters, void* ws, size_t ws_bytes, cudaStream_t s, int io) {
+                         uint32_t* status, int32_t* iters, unsigned* vcount, void* ws, size_t ws_bytes,
+                         cudaStream_t s, int io) {
   const float* in = static_cast<const float*>(in_v);  // io 0; raw pointers below go through in_v / out_v
   float* out = static_cast<float*>(out_v);
   const size_t isz = io ? 2 : 4, osz = io == 2 ? 2 : 4;
@@ -187,11 +206,15 @@ cudaError_t launch_fused(const void* in_v, void* out_v, int64_t B, int H, int W,
   p.dense = L.dense;
   p.md = c.max_depth;
   {
-    const int r = c.gaussian_size / 2;
+    // only the in-kernel Gaussian (size 5) uses these taps; every other blur
+    // mode (any gaussian_size up to 63) leaves them zero
     double w[5] = {0, 0, 0, 0, 0}, sum = 0;
-    for (int i = -r; i <= r; ++i) w[i + r] = std::exp(-(double)(i * i) / (2.0 * c.gaussian_sigma * c.gaussian_sigma));
-    for (int i = 0; i < 5; ++i) sum += w[i];
-    for (int i = 0; i < 5; ++i) p.gw[i] = (float)(w[i] / sum);
+    if (c.blur_mode == DFC_BLUR_GAUSSIAN && c.gaussian_size == 5) {
+      for (int i = -2; i <= 2; ++i)
+        w[i + 2] = std::exp(-(double)(i * i) / (2.0 * c.gaussian_sigma * c.gaussian_sigma));
+      for (int i = 0; i < 5; ++i) sum += w[i];
+    }
+    for (int i = 0; i < 5; ++i) p.gw[i] = sum > 0 ? (float)(w[i] / sum) : 0.f;
     for (int i = 0; i < 6; ++i)
       p.gh[i] = make_float2(i < 5 ? p.gw[i] : 0.f, i > 0 ? p.gw[i - 1] : 0.f);
   }
@@ -206,6 +229,7 @@ cudaError_t launch_fused(const void* in_v, void* out_v, int64_t B, int H, int W,
   p.umax = reinterpret_cast<unsigned*>(w8 + 16);
   cudaError_t e = cudaMemsetAsync(ws, 0, 16 + (size_t)B * 4, s);
   if (e != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(vcount, 0, (size_t)B * 8, s)) != cudaSuccess) return e;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -236,7 +260,8 @@ cudaError_t launch_fused(const void* in_v, void* out_v, int64_t B, int H, int W,
   }
   for (int64_t f0 = 0; f0 < B; f0 += chunk) {
     const int64_t C = B - f0 < chunk ? B - f0 : chunk;
-    if (pre && (e = launch_multiscale_stage2(in + f0 * HW, s2, C, H, W, c, op, on, umax0 + f0, s)) != cudaSuccess)
+    if (pre && (e = launch_multiscale_stage2(in + f0 * HW, s2, C, H, W, c, op, on, umax0 + f0, vcount + 2 * f0,
+                                             s)) != cudaSuccess)
       return e;
     char* out_c = static_cast<char*>(out_v) + f0 * HW * osz;
     p.in = pre ? (const void*)s2 : (const void*)(static_cast<const char*>(in_v) + f0 * HW * isz);
@@ -245,6 +270,7 @@ cudaError_t launch_fused(const void* in_v, void* out_v, int64_t B, int H, int W,
     p.status = status + f0;
     p.iters = iters ? iters + f0 : nullptr;
     p.umax = umax0 + f0;
+    p.vcount = vcount + 2 * f0;
     if (f0 > 0 && (e = cudaMemsetAsync(p.work, 0, 4, s)) != cudaSuccess) return e;
     const int64_t items = C * L.strips;
     const int64_t slots = (int64_t)sms * L.per_sm;
@@ -252,10 +278,12 @@ cudaError_t launch_fused(const void* in_v, void* out_v, int64_t B, int H, int W,
     // raw mode: the fused kernel writes float32 stage-6 maps; the blur tail encodes
     e = dispatch(vec, full, blur, pre, raw && io == 2 ? 1 : io, p, L.smem, grid, s);
     if (e != cudaSuccess) return e;
-    if (raw && (e = launch_blur_tail(tmp, out_c, C, H, W, c, io == 2, status + f0, s)) != cudaSuccess) return e;
+    if (raw && (e = launch_blur_tail(tmp, out_c, C, H, W, c, io == 2, status + f0, vcount + 2 * f0, s)) !=
+                   cudaSuccess)
+      return e;
   }
   note_launch();
-  finalize_kernel<<<(unsigned)B, 256, 0, s>>>(in, HW, umax0, status, c.max_depth, io != 0);
+  finalize_kernel<<<(unsigned)B, 256, 0, s>>>(in_v, HW, umax0, status, c.max_depth, io != 0, vcount, !pre);
   return cudaGetLastError();
 }
 

@@ -114,6 +114,7 @@ struct Params {
 #endif
   unsigned* work;
   unsigned* umax;
+  unsigned* vcount;  // [nframes][2]: inverted-valid inputs read (non-PRE), valid outputs stored (non-raw)
 };
 
 // Stage one lane's 4 columns of an input row into shared memory with cp.async
@@ -208,6 +209,12 @@ __device__ __forceinline__ void store_lane_t(T* q, const F4& a, unsigned colmask
         if (colmask >> c & 1u) q[c] = (uint16_t)enc_raw(a.v[c]);
     }
   }
+}
+
+// bits 0..3: the four columns hold a valid (> 0.1) value
+__device__ __forceinline__ unsigned valid_mask(const F4& a) {
+  return (unsigned)(a.v[0] > kValid) | (unsigned)(a.v[1] > kValid) << 1 | (unsigned)(a.v[2] > kValid) << 2 |
+         (unsigned)(a.v[3] > kValid) << 3;
 }
 
 // ---------------------------------------------------------------------------
@@ -643,6 +650,7 @@ struct State {
   long long tacc[6];   // diagnostics: producer, barrier, consumer, phase 1, consumer LF part, store-only rows
 #endif
   unsigned umax;
+  unsigned nin, nout;  // valid-pixel counters (owned output columns): inputs read, outputs stored
   bool had_empty, still_empty;
   uint32_t mbW, mbL, mbR;  // shared addresses of this warp's / the neighbours' P[4], C[4] mbarriers
   bool hasL, hasR;
@@ -684,6 +692,10 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
         a[j].v[1] = a[j].v[1] > kValid ? d01.y : 0.0f;
         a[j].v[2] = a[j].v[2] > kValid ? d23.x : 0.0f;
         a[j].v[3] = a[j].v[3] > kValid ? d23.y : 0.0f;
+        // RunStats.input_density (pipeline.py:138-141): inverted-valid inputs of the
+        // owned output columns; each row is read once (rows outside the frame are 0)
+        S.nin += __popc(((unsigned)(a[j].v[0] > kValid) | (unsigned)(a[j].v[1] > kValid) << 1 |
+                         (unsigned)(a[j].v[2] > kValid) << 2 | (unsigned)(a[j].v[3] > kValid) << 3) & S.outm);
       }
     }
     // stage the next block; stops once its stage-5 rows lie above every r0.
@@ -871,6 +883,7 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
       const int t = tc0 - 2 + j;
       if (EDGE && (t < 0 || t >= H)) continue;
       if (S.outm) store_lane_t<VEC>(orow, S.ofast, S.outm, S.enc_over);
+      if (BLUR != kBlurRaw) S.nout += __popc(valid_mask(S.ofast) & S.outm);
     }
     break;
   }
@@ -1053,6 +1066,7 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
         if (!FULL && !(mk[j].v[c + 1] > kValid)) o.v[c + 1] = 0.0f;
       }
       if (S.outm) store_lane_t<VEC>(orow, o, S.outm, S.enc_over);
+      S.nout += __popc(valid_mask(o) & S.outm);
     }
     // rows tc0-4 .. tc0+3 above every needed r0: output row tc0+1 repeats from here on
     if (FULL && !EDGE && tc0 - 4 > S.tmaxN) {
@@ -1070,6 +1084,7 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
       for (int c = 0; c < 4; ++c)
         o.v[c] = BLUR == kBlurRaw ? v6[j].v[c] : (v6[j].v[c] > kValid ? p.md - v6[j].v[c] : 0.0f);
       if (S.outm) store_lane_t<VEC>(orow, o, S.outm, S.enc_over);
+      if (BLUR != kBlurRaw) S.nout += __popc(valid_mask(o) & S.outm);
     }
     if (FULL && !EDGE && tc0 > S.tmaxN) {
       S.fast = true;
@@ -1156,6 +1171,7 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
     S.edgeL = S.x0 == 0;                                           // lane holding column 0
     S.compR = (S.x0 <= W - 1 && W - 1 <= S.x0 + 3) ? W - 1 - S.x0 : -1;  // component of column W - 1
     S.umax = 0;
+    S.nin = S.nout = 0;
     S.had_empty = S.still_empty = false;
     S.skip = S.fast = S.enc_over = false;
     S.mbW = mb0 + warp * 64;
@@ -1247,11 +1263,14 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
     gk = S.gk;
     // ---------------- per-frame flags ----------------
     const unsigned um = __reduce_max_sync(kFull, S.umax);
+    const unsigned nin = __reduce_add_sync(kFull, S.nin), nout = __reduce_add_sync(kFull, S.nout);
     const bool he = __any_sync(kFull, S.had_empty);
     const bool se = __any_sync(kFull, S.still_empty);
     const bool eo = IO == 2 && __any_sync(kFull, S.enc_over);
     if (lane == 0) {
       if (!PRE) atomicMax(p.umax + frame, um);  // PRE: multiscale.cu records it
+      if (!PRE && nin) atomicAdd(p.vcount + 2 * frame, nin);  // PRE: multiscale.cu counts the inputs
+      if (BLUR != kBlurRaw && nout) atomicAdd(p.vcount + 2 * frame + 1, nout);  // raw: the blur tail counts
       if (eo) atomicOr(p.status + frame, DFC_ST_ENCODE);
       if (FULL && he && p.iters) atomicOr(p.iters + frame, 1);
       if (FULL && se) {

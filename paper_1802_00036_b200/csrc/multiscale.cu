@@ -39,6 +39,7 @@ struct BinParams {
 template <int R>
 __global__ void __launch_bounds__(kThreads) ms_stage2_kernel(const float* __restrict__ in, float* __restrict__ out,
                                                              int H, int W, unsigned* __restrict__ umax,
+                                                             unsigned* __restrict__ vcount,
                                                              const __grid_constant__ BinParams p) {
   constexpr int IW = kTX + 2 * R, IH = kTY + 2 * R;
   __shared__ float sb[3][IH * IW];
@@ -47,20 +48,24 @@ __global__ void __launch_bounds__(kThreads) ms_stage2_kernel(const float* __rest
   const int x0 = blockIdx.x * kTX, y0 = blockIdx.y * kTY;
   const float* src = in + b * (int64_t)H * W;
   if (threadIdx.x == 0) s_umax = 0;
-  unsigned um = 0;
+  unsigned um = 0, nv = 0;
   for (int i = threadIdx.x; i < IH * IW; i += kThreads) {
     const int iy = i / IW, ix = i - iy * IW;
     const int gy = y0 - R + iy, gx = x0 - R + ix;
     const float d = __ldg(src + (int64_t)clampi(gy, H) * W + clampi(gx, W));
     if (gy >= 0 && gy < H && gx >= 0 && gx < W) um = max(um, __float_as_uint(d));
+    // valid inputs of the tile itself (each pixel in exactly one tile)
+    if (iy >= R && iy < R + kTY && ix >= R && ix < R + kTX && gy < H && gx < W) nv += d > kValid;
     const float v = d > kValid ? p.md - d : 0.0f;  // depth_core.invert
     sb[0][i] = d <= p.edge_near ? v : 0.0f;
     sb[1][i] = (d > p.edge_near && d <= p.edge_far) ? v : 0.0f;
     sb[2][i] = d > p.edge_far ? v : 0.0f;
   }
   um = __reduce_max_sync(0xffffffffu, um);
+  nv = __reduce_add_sync(0xffffffffu, nv);
   __syncthreads();
   if ((threadIdx.x & 31) == 0) atomicMax(&s_umax, um);
+  if ((threadIdx.x & 31) == 0 && nv) atomicAdd(vcount + 2 * b, nv);
   float* dst = out + b * (int64_t)H * W;
   for (int i = threadIdx.x; i < kTX * kTY; i += kThreads) {
     const int oy = i / kTX, ox = i - oy * kTX;
@@ -129,6 +134,7 @@ constexpr int kTmNc = 0, kTmM1 = 24, kTmM2 = 32, kTmM3 = 40, kTmF1 = 48, kTmF2 =
 struct MsState {
   F4 fd, nx[kB];
   unsigned um;
+  unsigned nv;  // valid inputs (> 0.1) of the owned columns: RunStats.input_density (pipeline.py:138-141)
   uint32_t tm;  // this thread's TMEM lane, column 0
 };
 
@@ -153,6 +159,7 @@ __device__ __forceinline__ void ms_block(MsState& S, const float* __restrict__ s
     for (int c = 0; c < 4; ++c) {
       const float v = cur[j].v[c];
       S.um = max(S.um, __float_as_uint(v));
+      S.nv += (own >> c & 1u) && v > kValid;  // rows outside the frame are 0
       const float inv = v > kValid ? p.md - v : 0.0f;  // depth_core.invert
       const bool near = v <= p.edge_near, far = v > p.edge_far;
       nv[j].v[c] = near ? inv : 0.0f;
@@ -224,8 +231,8 @@ __device__ __forceinline__ void ms_rows(MsState& S, const float* src, float* dst
 
 template <int VEC>
 __device__ __forceinline__ void ms_warp(const float* __restrict__ in, float* __restrict__ out, int H, int W,
-                                        unsigned* __restrict__ umax, const MsFastParams& p, int S0, int lane,
-                                        uint32_t tm) {
+                                        unsigned* __restrict__ umax, unsigned* __restrict__ vcount,
+                                        const MsFastParams& p, int S0, int lane, uint32_t tm) {
   const int64_t b = blockIdx.y;
   const float* src = in + b * (int64_t)H * W;
   float* dst = out + b * (int64_t)H * W;
@@ -252,6 +259,7 @@ __device__ __forceinline__ void ms_warp(const float* __restrict__ in, float* __r
   }
   set_row(S.fd, 0.f);
   S.um = 0;
+  S.nv = 0;
 #pragma unroll
   for (int j = 0; j < kB; ++j) {
     if (j < H)
@@ -264,13 +272,16 @@ __device__ __forceinline__ void ms_warp(const float* __restrict__ in, float* __r
   else
     ms_rows<VEC, false>(S, src, dst, H, W, x0, oob, own, p);
   const unsigned um = __reduce_max_sync(kFull, S.um);
+  const unsigned nv = __reduce_add_sync(kFull, S.nv);
   if (lane == 0) atomicMax(umax + b, um);
+  if (lane == 0 && nv) atomicAdd(vcount + 2 * b, nv);
 }
 
 template <int VEC>
 __global__ void __launch_bounds__(kMsWarps * 32, 4) ms_fast_kernel(const float* __restrict__ in,
                                                                    float* __restrict__ out, int H, int W,
                                                                    unsigned* __restrict__ umax,
+                                                                   unsigned* __restrict__ vcount,
                                                                    const __grid_constant__ MsFastParams p) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   static_assert(kMsWarps == 4, "one warp per TMEM lane quarter");
@@ -281,7 +292,7 @@ __global__ void __launch_bounds__(kMsWarps * 32, 4) ms_fast_kernel(const float* 
   tm_fence_after();
   const uint32_t tmbase = s_tm;
   const int S0 = (blockIdx.x * kMsWarps + warp) * kMsOwn;
-  if (S0 < W) ms_warp<VEC>(in, out, H, W, umax, p, S0, lane, tmbase + ((uint32_t)(warp * 32) << 16));
+  if (S0 < W) ms_warp<VEC>(in, out, H, W, umax, vcount, p, S0, lane, tmbase + ((uint32_t)(warp * 32) << 16));
   tm_wait_st();
   tm_fence_before();
   __syncthreads();
@@ -304,17 +315,18 @@ bool multiscale_stage2_supported(const dfc_config& c) {
 }
 
 cudaError_t launch_multiscale_stage2(const float* in, float* out, int64_t B, int H, int W, const dfc_config& c,
-                                     const int32_t* const offs[3], const int n[3], unsigned* umax, cudaStream_t s) {
+                                     const int32_t* const offs[3], const int n[3], unsigned* umax, unsigned* vcount,
+                                     cudaStream_t s) {
   if (multiscale_fast_kernels(c)) {
     MsFastParams q{c.max_depth, c.bin_edge_near, c.bin_edge_far};
     const dim3 grid((unsigned)((W + kMsOwn * kMsWarps - 1) / (kMsOwn * kMsWarps)), (unsigned)B);
     note_launch();
     if (W % 4 == 0)
-      ms_fast_kernel<4><<<grid, kMsWarps * 32, 0, s>>>(in, out, H, W, umax, q);
+      ms_fast_kernel<4><<<grid, kMsWarps * 32, 0, s>>>(in, out, H, W, umax, vcount, q);
     else if (W % 2 == 0)
-      ms_fast_kernel<2><<<grid, kMsWarps * 32, 0, s>>>(in, out, H, W, umax, q);
+      ms_fast_kernel<2><<<grid, kMsWarps * 32, 0, s>>>(in, out, H, W, umax, vcount, q);
     else
-      ms_fast_kernel<1><<<grid, kMsWarps * 32, 0, s>>>(in, out, H, W, umax, q);
+      ms_fast_kernel<1><<<grid, kMsWarps * 32, 0, s>>>(in, out, H, W, umax, vcount, q);
     return cudaGetLastError();
   }
   BinParams p{};
@@ -335,9 +347,9 @@ cudaError_t launch_multiscale_stage2(const float* in, float* out, int64_t B, int
   note_launch();
   switch (R) {
     case 0:
-    case 1: ms_stage2_kernel<1><<<grid, kThreads, 0, s>>>(in, out, H, W, umax, p); break;
-    case 2: ms_stage2_kernel<2><<<grid, kThreads, 0, s>>>(in, out, H, W, umax, p); break;
-    case 3: ms_stage2_kernel<3><<<grid, kThreads, 0, s>>>(in, out, H, W, umax, p); break;
+    case 1: ms_stage2_kernel<1><<<grid, kThreads, 0, s>>>(in, out, H, W, umax, vcount, p); break;
+    case 2: ms_stage2_kernel<2><<<grid, kThreads, 0, s>>>(in, out, H, W, umax, vcount, p); break;
+    case 3: ms_stage2_kernel<3><<<grid, kThreads, 0, s>>>(in, out, H, W, umax, vcount, p); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

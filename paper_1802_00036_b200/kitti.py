@@ -67,6 +67,8 @@ def colormap(values, range_min: float, range_max: float) -> torch.Tensor:
     v = values if isinstance(values, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(values, np.float32))
     if v.device.type != "cuda":
         v = v.to(_device())
+    if v.dtype != torch.float32:  # dfc_colormap reads float32
+        v = v.to(torch.float32)
     v = v.contiguous()
     rgb = torch.empty(tuple(v.shape) + (3,), dtype=torch.uint8, device=v.device)
     _lib.check(_lib.load().dfc_colormap(ops._ptr(v), ops._ptr(rgb), v.numel(), float(range_min), float(range_max),

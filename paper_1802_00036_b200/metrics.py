@@ -57,6 +57,8 @@ def _as_batch(x) -> torch.Tensor:
         x = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32))
     if x.device.type != "cuda":
         x = x.to(_device())
+    if x.dtype != torch.float32:  # the kernels read float32 (metrics.py:110-117 works on float32 maps)
+        x = x.to(torch.float32)
     x = x.contiguous()
     return x.unsqueeze(0) if x.dim() == 2 else x
 

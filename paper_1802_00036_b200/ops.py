@@ -8,6 +8,7 @@ computes on the CPU: a missing libdfc.so or CUDA device raises.
 from __future__ import annotations
 
 import ctypes
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -182,27 +183,69 @@ class FillResult:
     dense: torch.Tensor        # [B, H, W] float32, direct encoding
     status: torch.Tensor       # [B] int32 DFC_ST_* bits
     iterations: torch.Tensor   # [B] int32 large-fill iterations
+    valid_counts: torch.Tensor | None = None  # [B, 2] int32: input / output pixels > 0.1 (RunStats densities)
+
+    def densities(self) -> tuple[np.ndarray, np.ndarray]:
+        """RunStats.input_density / output_density per frame (pipeline.py:138-141, 192-202)."""
+        if self.valid_counts is None:
+            raise ValueError("no valid-pixel counts for this result")
+        n = self.dense.shape[-1] * self.dense.shape[-2]
+        c = self.valid_counts.cpu().numpy().astype(np.int64)
+        return c[:, 0] / n, c[:, 1] / n
 
 
 class Workspace:
-    """Reusable device workspace for dfc_fill_batch (grown on demand)."""
+    """Device workspace for dfc_fill_batch, grown on demand.
+
+    A workspace belongs to one stream at a time: the library keeps per-call
+    counters in it (work queue, fallback count, validation maxima), so two
+    calls in flight on different streams must not share one.  The default
+    workspaces are therefore keyed by (device, stream) and locked for the
+    duration of a call; a buffer dropped on growth is first recorded on the
+    stream that last used it, so the caching allocator cannot hand it out
+    while that stream's kernels may still read it.
+    """
 
     def __init__(self):
         self.buf = None
+        self.stream = None  # the stream of the last call that used buf
+        self.lock = threading.Lock()
 
     def get(self, nbytes: int, device) -> torch.Tensor:
+        """The buffer for a call about to run on torch's current stream of ``device``."""
+        cur = torch.cuda.current_stream(device)
         if self.buf is None or self.buf.numel() < nbytes or self.buf.device != device:
+            if self.buf is not None and self.stream is not None:
+                self.buf.record_stream(self.stream)
             self.buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+        elif self.stream is not None and self.stream != cur:
+            # reused on another stream: keep the allocator from recycling it
+            # while the earlier stream may still be running on it
+            self.buf.record_stream(cur)
+            cur.wait_stream(self.stream)
+        self.stream = cur
         return self.buf
 
 
-_default_ws = {}
+_default_ws: dict = {}
+_default_ws_lock = threading.Lock()
+
+
+def _workspace_for(device) -> Workspace:
+    """The default workspace of (device, current stream)."""
+    key = (device, torch.cuda.current_stream(device).cuda_stream)
+    with _default_ws_lock:
+        ws = _default_ws.get(key)
+        if ws is None:
+            ws = _default_ws[key] = Workspace()
+    return ws
 
 
 def fill_batch(frames: torch.Tensor, cfg: "_lib.DfcConfig", out: torch.Tensor | None = None,
                workspace: Workspace | None = None, status: torch.Tensor | None = None,
-               iterations: torch.Tensor | None = None) -> FillResult:
-    """Run the depth-completion pipeline on B frames via dfc_fill_batch."""
+               iterations: torch.Tensor | None = None, counts: bool = True) -> FillResult:
+    """Run the depth-completion pipeline on B frames via dfc_fill_batch (and
+    dfc_fill_counts for the per-frame valid-pixel counts unless counts=False)."""
     x, _ = _as_batch(frames)
     B, H, W = x.shape
     L = _lib.load()
@@ -211,17 +254,21 @@ def fill_batch(frames: torch.Tensor, cfg: "_lib.DfcConfig", out: torch.Tensor | 
         # invalid config: let dfc_fill_batch report the reason
         check(L.dfc_fill_batch(None, None, B, H, W, ctypes.byref(cfg), None, None, None, 0, _stream()))
     if workspace is None:
-        workspace = _default_ws.setdefault(x.device, Workspace())
-    ws = workspace.get(need, x.device)
+        workspace = _workspace_for(x.device)
     if out is None:
         out = torch.empty_like(x)
     if status is None:
         status = torch.empty(B, dtype=torch.int32, device=x.device)
     if iterations is None:
         iterations = torch.empty(B, dtype=torch.int32, device=x.device)
-    check(L.dfc_fill_batch(_ptr(x), _ptr(out), B, H, W, ctypes.byref(cfg), _ptr(status), _ptr(iterations),
-                           _ptr(ws), ws.numel(), _stream()))
-    return FillResult(out, status, iterations)
+    vc = torch.empty((B, 2), dtype=torch.int32, device=x.device) if counts else None
+    with workspace.lock:
+        ws = workspace.get(need, x.device)
+        check(L.dfc_fill_batch(_ptr(x), _ptr(out), B, H, W, ctypes.byref(cfg), _ptr(status), _ptr(iterations),
+                               _ptr(ws), ws.numel(), _stream()))
+        if counts and B > 0 and not (cfg.flags & _lib.F_NO_FINISH):
+            check(L.dfc_fill_counts(ctypes.byref(cfg), B, H, W, _ptr(ws), ws.numel(), _ptr(vc), _stream()))
+    return FillResult(out, status, iterations, vc if counts and not (cfg.flags & _lib.F_NO_FINISH) else None)
 
 
 # ---------------------------------------------------------------------------
@@ -244,16 +291,17 @@ def fill_batch_raw16(raw: torch.Tensor, cfg: "_lib.DfcConfig", out_raw: bool = T
         check(L.dfc_fill_batch_raw16(None, None, int(out_raw), B, H, W, ctypes.byref(cfg), None, None, None, 0,
                                      _stream()))
     if workspace is None:
-        workspace = _default_ws.setdefault(x.device, Workspace())
-    ws = workspace.get(need, x.device)
+        workspace = _workspace_for(x.device)
     if out is None:
         out = torch.empty(x.shape, dtype=torch.uint16 if out_raw else torch.float32, device=x.device)
     if status is None:
         status = torch.empty(B, dtype=torch.int32, device=x.device)
     if iterations is None:
         iterations = torch.empty(B, dtype=torch.int32, device=x.device)
-    check(L.dfc_fill_batch_raw16(_ptr(x), _ptr(out), int(out_raw), B, H, W, ctypes.byref(cfg), _ptr(status),
-                                 _ptr(iterations), _ptr(ws), ws.numel(), _stream()))
+    with workspace.lock:
+        ws = workspace.get(need, x.device)
+        check(L.dfc_fill_batch_raw16(_ptr(x), _ptr(out), int(out_raw), B, H, W, ctypes.byref(cfg), _ptr(status),
+                                     _ptr(iterations), _ptr(ws), ws.numel(), _stream()))
     return FillResult(out, status, iterations)
 
 

@@ -14,6 +14,8 @@ and stores its outputs:
                             from their seeds and also hashed),
 * ``multiscale_small.npz`` -- the composed multiscale oracle built from the
                             reference's own morphology.dilate per depth bin,
+* ``multiscale_full.json`` -- full-size BASELINE config 2 / 4 frames through the
+                            composed multiscale oracle: sha256 of the output,
 * ``metrics_small.npz`` / ``metrics_small.json`` -- metrics.evaluate, error_map
                             and MetricsAccumulator on seeded prediction / ground
                             truth pairs,
@@ -23,7 +25,7 @@ and stores its outputs:
 
 Nothing here is copied from a dataset; every input is generated from a seed.
 Usage:  python tests/golden/make_golden.py [name ...]   (needs /root/reference;
-        names: ops stages pipeline multiscale full metrics kitti; default all)
+        names: ops stages pipeline multiscale full metrics kitti multiscale_full; default all)
 """
 
 from __future__ import annotations
@@ -367,8 +369,28 @@ def gen_kitti():
     np.savez_compressed(HERE / "kitti_small.npz", **out)
 
 
+# full-size BASELINE fill_in_multiscale frames (config 2: 1216x352, config 4:
+# 4096x1024 with max_depth 120), pinned by SHA-256 of the composed reference output
+MS_FULL_CASES = [(2, 0, 100.0), (2, 1, 100.0), (4, 0, 120.0)]
+
+
+def gen_multiscale_full():
+    meta = []
+    for (c, i, off) in MS_FULL_CASES:
+        v = synth.make_frame(synth.CONFIG_SPECS[c], [c, i])
+        dense, it = ref_multiscale(v, MS_KERNELS[0], "median_bilateral", off)
+        meta.append({"config": c, "frame": i, "kernels": MS_KERNELS[0], "edges": MS_EDGES,
+                     "blur": "median_bilateral", "offset": off, "input_sha256": sha(v),
+                     "output_sha256": sha(dense), "iters": it,
+                     "samples": [[int(y), int(x), float(dense[y, x])]
+                                 for y, x in ((0, 0), (v.shape[0] // 2, v.shape[1] // 2),
+                                              (v.shape[0] - 1, v.shape[1] - 1), (150, 600))]})
+    (HERE / "multiscale_full.json").write_text(json.dumps(meta, indent=1))
+
+
 GENS = {"ops": gen_ops, "stages": gen_stages, "pipeline": gen_pipeline_small, "multiscale": gen_multiscale,
-        "full": gen_pipeline_full, "metrics": gen_metrics, "kitti": gen_kitti}
+        "full": gen_pipeline_full, "metrics": gen_metrics, "kitti": gen_kitti,
+        "multiscale_full": gen_multiscale_full}
 
 if __name__ == "__main__":
     for name in sys.argv[1:] or list(GENS):

@@ -71,3 +71,19 @@ def test_metrics_errors(Mx):
         Mx.evaluate(np.zeros((4, 5), np.float32), np.ones((4, 5), np.float32))
     with pytest.raises(ValueError, match="no overlapping"):
         Mx.MetricsAccumulator().finalize()
+
+
+def test_metrics_non_float32_tensors(Mx):
+    """float64 / float16 CUDA tensors are converted, not reinterpreted as float32 bits."""
+    rng = np.random.default_rng(5)
+    p = rng.uniform(1, 80, (30, 40)).astype(np.float32)
+    g = rng.uniform(1, 80, (30, 40)).astype(np.float32)
+    g[rng.random(g.shape) < 0.3] = 0
+    want = Mx.error_sums(p, g)
+    got = Mx.error_sums(torch.from_numpy(p.astype(np.float64)).cuda(), torch.from_numpy(g.astype(np.float64)).cuda())
+    assert np.array_equal(want[0], got[0]) and np.array_equal(want[1], got[1])
+    from paper_1802_00036_b200 import kitti
+
+    a = kitti.colormap(torch.from_numpy(p).cuda(), 0.0, 80.0).cpu()
+    b = kitti.colormap(torch.from_numpy(p.astype(np.float64)).cuda(), 0.0, 80.0).cpu()
+    assert torch.equal(a, b)

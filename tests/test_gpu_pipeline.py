@@ -445,3 +445,81 @@ def test_randomized_configs_vs_oracle(P, case):
         assert not st[i] & 0xFF, st[i]
         _cmp(got[i], ref, blur)
         assert int(res.iterations[i]) == info["large_fill_iterations"]
+
+
+def _counts_ref(frames, ocfg):
+    out = []
+    for f in frames:
+        _, info = O.complete_with_stats(f, ocfg)
+        n = f.size
+        out.append((round(info["input_density"] * n), round(info["output_density"] * n)))
+    return np.array(out)
+
+
+@pytest.mark.parametrize("blur,fill,multi,staged", [("gaussian", "full", False, False),
+                                                    ("bilateral", "partial", False, False),
+                                                    ("median_bilateral", "full", True, False),
+                                                    ("none", "full", False, False),
+                                                    ("gaussian", "partial", False, True)])
+def test_density_counters_vs_oracle(P, blur, fill, multi, staged):
+    """(f)3: per-frame valid-pixel counts from the fused read / store passes
+    (dfc_fill_counts) equal RunStats' input / output densities times H*W
+    (pipeline.py:138-141, 192-202) exactly -- including frames with inputs
+    within 0.1 of max_depth (valid, but invalid once inverted) and a frame
+    finished by the staged fallback."""
+    frames = synth.make_batch(1, 800, 6)
+    frames[2][frames[2] > 0] = np.float32(99.95)  # every valid input inverts to an empty pixel
+    frames[3].flat[::97] = np.float32(99.95)
+    f4 = np.zeros_like(frames[4])
+    f4[100, 50] = 20.0
+    f4[300, 1100] = 40.0
+    frames[4] = f4  # needs many large-fill iterations (staged fallback in FULL mode)
+    kw = {"blur_mode": blur, "fill_mode": fill}
+    ocfg = _ocfg(kw)
+    if multi:
+        ocfg = O.OracleConfig(**{**ocfg.__dict__, "multiscale": MS_DEFAULT})
+    res = P.complete_batch(frames, _pcfg(P, kw), multiscale=P.MultiscaleConfig() if multi else None,
+                           force_staged=staged, raise_on_error=False)
+    got = res.valid_counts.cpu().numpy()
+    ok = [i for i in range(6) if not res.status.cpu().numpy()[i] & 0xFF]
+    want = _counts_ref(frames[ok], ocfg)
+    assert np.array_equal(got[ok], want), (got[ok], want)
+    din, dout = res.densities()
+    assert np.allclose(din[ok] * frames[0].size, want[:, 0])
+
+
+@pytest.mark.parametrize("blur", ["none", "bilateral", "median"])
+@pytest.mark.parametrize("gsize", [7, 63])
+def test_fused_path_other_blur_any_gaussian_size(P, blur, gsize):
+    """gaussian_size only matters to the Gaussian: the fused path with another blur
+    and a non-default gaussian_size runs and matches the oracle."""
+    frames = synth.make_batch(1, 850, 2)
+    kw = {"blur_mode": blur, "fill_mode": "full", "gaussian_size": gsize}
+    res = P.complete_batch(frames, _pcfg(P, kw))
+    got = res.dense.cpu().numpy()
+    for i in range(2):
+        ref = O.complete(frames[i], _ocfg(kw))
+        _cmp(got[i], ref, blur)
+
+
+def test_sparse_batch_fallback_batched(P):
+    """A batch of very sparse frames (uniform ~0.05 % points: many large-fill
+    iterations each) goes through the batched, device-gated fallback: every
+    frame matches the oracle with its own iteration count."""
+    rng = np.random.default_rng(123)
+    n = 40
+    frames = np.zeros((n, 352, 1216), np.float32)
+    for i in range(n):
+        m = rng.random(frames[i].shape) < rng.uniform(0.0002, 0.001)
+        frames[i][m] = rng.uniform(1, 90, m.sum()).astype(np.float32)
+    kw = {"blur_mode": "gaussian", "fill_mode": "full"}
+    res = P.complete_batch(frames, _pcfg(P, kw))
+    got = res.dense.cpu().numpy()
+    st = res.status.cpu().numpy()
+    its = res.iterations.cpu().numpy()
+    assert (st & 0x100).sum() > n // 2, "expected most frames on the fallback"
+    for i in range(0, n, 5):
+        ref, info = O.complete_with_stats(frames[i], _ocfg(kw))
+        _cmp(got[i], ref, "gaussian")
+        assert int(its[i]) == info["large_fill_iterations"]
+    assert len(set(its.tolist())) > 1

@@ -127,6 +127,25 @@ def test_pipeline_full_golden(golden_dir, case):
     assert info["large_fill_iterations"] == meta["iters"]
 
 
+def _ms_cfg(m):
+    (sn, zn), (sm, zm), (sf, zf) = m["kernels"]
+    ms = (tuple(m["edges"]), (O.KernelShape(sn), zn), (O.KernelShape(sm), zm), (O.KernelShape(sf), zf))
+    return O.OracleConfig(blur_mode=O.BlurMode(m["blur"]), multiscale=ms, max_depth=m["offset"])
+
+
+@pytest.mark.parametrize("case", range(3))
+def test_multiscale_full_golden(golden_dir, case):
+    """BASELINE config 2 / 4 full-size frames (4096x1024, max_depth 120 for config 4)
+    through the composed multiscale oracle, pinned by SHA-256 to the composition of
+    the reference's own primitives (make_golden.py: ref_multiscale)."""
+    m = json.loads((golden_dir / "multiscale_full.json").read_text())[case]
+    v = synth.make_frame(synth.CONFIG_SPECS[m["config"]], [m["config"], m["frame"]])
+    assert hashlib.sha256(v.tobytes()).hexdigest() == m["input_sha256"], "generator drifted"
+    dense, info = O.complete_with_stats(v, _ms_cfg(m))
+    assert hashlib.sha256(dense.tobytes()).hexdigest() == m["output_sha256"]
+    assert info["large_fill_iterations"] == m["iters"]
+
+
 def test_metrics_oracle_matches_reference(golden_dir):
     """oracle/metrics_oracle.py against depthfill.metrics outputs."""
     from oracle import metrics_oracle as M

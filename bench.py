@@ -42,18 +42,20 @@ UNIT = "frames/s"
 CONFIG_ID = 1
 
 
-# BASELINE.json configs: (blur, fill, multiscale, default frames per GPU, call)
+# BASELINE.json configs: (blur, fill, multiscale, default frames, call, scaling).  "weak": the
+# frames are per GPU; "strong": the frames are the whole batch, split over the GPUs (config 3:
+# "Batch of 8192 frames ... sharded by frame index across 1, 2, 4 and 8 B200s").
 CONFIGS = {
     0: ("bilateral", "partial", False, 1024,
-        "fill_in_fast(max_depth=100, 5x5 diamond, extrapolate=False, blur_type='bilateral')"),
+        "fill_in_fast(max_depth=100, 5x5 diamond, extrapolate=False, blur_type='bilateral')", "weak"),
     1: ("gaussian", "full", False, 1024,
-        "fill_in_fast(max_depth=100, 5x5 diamond, extrapolate=True, blur_type='gaussian')"),
+        "fill_in_fast(max_depth=100, 5x5 diamond, extrapolate=True, blur_type='gaussian')", "weak"),
     2: ("median_bilateral", "full", True, 1024,
-        "fill_in_multiscale(max_depth=100, extrapolate=True, blur_type='bilateral', median_blur=True)"),
-    3: ("gaussian", "full", False, 1024,
-        "fill_in_fast(max_depth=100, 5x5 diamond, extrapolate=True, blur_type='gaussian')"),
+        "fill_in_multiscale(max_depth=100, extrapolate=True, blur_type='bilateral', median_blur=True)", "weak"),
+    3: ("gaussian", "full", False, 8192,
+        "fill_in_fast(max_depth=100, 5x5 diamond, extrapolate=True, blur_type='gaussian')", "strong"),
     4: ("median_bilateral", "full", True, 256,
-        "fill_in_multiscale(max_depth=120, extrapolate=True, blur_type='bilateral', median_blur=True)"),
+        "fill_in_multiscale(max_depth=120, extrapolate=True, blur_type='bilateral', median_blur=True)", "weak"),
 }
 
 
@@ -65,7 +67,10 @@ def parse():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--config", type=int, default=1, choices=sorted(CONFIGS),
                    help="BASELINE.json config (1 = the headline metric; the others are extra measurements)")
-    p.add_argument("--frames", type=int, default=None, help="frames per rank per step (default: per config)")
+    p.add_argument("--frames", type=int, default=None,
+                   help="frames per rank per step (weak scaling; default: per config)")
+    p.add_argument("--total-frames", type=int, default=None,
+                   help="frames of the whole batch, split over the ranks (strong scaling; config 3 default 8192)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU-baseline sample length")
@@ -257,9 +262,12 @@ def config_block(B, args):
     sp = synth.CONFIG_SPECS[CONFIG_ID]
     dens = (f"{sp.density[0]:.0%}" if sp.density[0] == sp.density[1]
             else f"U({sp.density[0]:.0%},{sp.density[1]:.0%})")
-    return {"workload": f"BASELINE config {CONFIG_ID}: {CONFIGS[CONFIG_ID][4]} on {B} synthetic "
-                        f"{sp.width}x{sp.height} frames per GPU",
-            "config_id": CONFIG_ID, "frames_per_gpu": B, "width": sp.width, "height": sp.height, "density": dens,
+    batch = (f"a {args.total_frames}-frame batch split over {args.gpus} GPU(s) ({B} per GPU)" if args.total_frames
+             else f"{B} synthetic frames per GPU")
+    return {"workload": f"BASELINE config {CONFIG_ID}: {CONFIGS[CONFIG_ID][4]} on {batch}, "
+                        f"{sp.width}x{sp.height}",
+            "config_id": CONFIG_ID, "frames_per_gpu": B, "total_frames": args.total_frames,
+            "width": sp.width, "height": sp.height, "density": dens,
             "l2": "no flush needed: each step streams 2 x %.2f GB (> 126 MB L2)" % (B * sp.width * sp.height * 4 / 1e9),
             "parallelism": f"frame-sharded dp{args.gpus}, no collective",
             "path": ("reference CPU (oracle/_ref compiled reference kernels)" if args.impl == "reference"
@@ -272,12 +280,19 @@ def run_reference(args):
         return
     from oracle import cpu_baseline as C
 
-    frames = gen_frames(0, 64 if CONFIG_ID != 4 else 8)
     cfg = oracle_config()
     procs = os.cpu_count() or 1
-    pool, procs, kind = C.make_pool(frames, cfg, procs)
-    per_step = 2 * procs
+    kind = C.available_kind()
+    # one step = the GPU arm's per-GPU batch (same frames, same config), unless that
+    # would take more than ~3 s of the box's cores: then a bounded sample of it
+    probe = gen_frames(0, 1)
+    one = C.single_frame_seconds(probe[0], cfg, kind)
+    B = args.frames
+    per_step = int(min(B, max(2 * procs, 3.0 * procs / max(one, 1e-4))))
+    frames = gen_frames(0, per_step)
+    pool, procs, kind = C.make_pool(frames, cfg, procs, kind)
     try:
+        pool.map(C._work, range(procs), chunksize=1)  # warm every worker
         for _ in range(args.warmup):
             pool.map(C._work, range(per_step), chunksize=1)
         t0 = time.perf_counter()
@@ -292,9 +307,12 @@ def run_reference(args):
             "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, SURVEY 8(d))",
             "impl": "reference",
-            "config": {**config_block(args.frames, args), "reference_step": f"{per_step} frames per step"},
+            "config": {**config_block(args.frames, args), "reference_step": f"{per_step} frames per step",
+                       "same_config": per_step == B},
             "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": procs, "kind": kind,
-                             "sample": f"{per_step} frames/step x {args.steps} steps over {len(frames)} distinct frames",
+                             "sample": f"{per_step} distinct frames per step (one pool.map over {procs} "
+                                       f"single-threaded processes) x {args.steps} steps; single-thread "
+                                       f"{one * 1e3:.1f} ms/frame",
                              "cpu_model": _cpu_model()},
             "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -323,8 +341,11 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    B = args.frames
-    f0, f1 = frame_range(rank, world, per_rank=B)  # weak scaling: B frames per GPU, disjoint ranges
+    if args.total_frames:  # strong scaling: one batch split over the ranks
+        f0, f1 = frame_range(rank, world, total=args.total_frames)
+    else:  # weak scaling: B frames per GPU, disjoint ranges
+        f0, f1 = frame_range(rank, world, per_rank=args.frames)
+    B = f1 - f0
     host = gen_frames(f0, f1 - f0)
     x = torch.from_numpy(host).to(dev)
     out = torch.empty_like(x)
@@ -382,13 +403,17 @@ def run_ours(args):
     clk = clocks.stop(window=(th0, th1))
     elapsed_ms, kern_ms = max_over_ranks([elapsed_ms, kern_ms], device=dev)
     ms_step = elapsed_ms / args.steps
-    value = world * B * args.steps / (elapsed_ms / 1e3)
+    job_frames = args.total_frames or world * B  # frames all ranks processed per step
+    value = job_frames * args.steps / (elapsed_ms / 1e3)
 
     # ---- e2e: host buffers through the public API -------------------------
     e2e = None
+    # host memory: the e2e legs pin copies of the inputs and outputs; above
+    # 4 GB of frames per rank they run on the first 4 GB worth (stated in the line)
+    e2e_n = min(B, max(1, (4 << 30) // (W * H * 4)))
     if not args.no_e2e:
         pipe = HostPipeline(config, multiscale=ms, chunk=64 if W * H < 1 << 20 else 8)
-        h_in = torch.from_numpy(host).pin_memory()
+        h_in = torch.from_numpy(host[:e2e_n]).pin_memory()
         h_out = torch.empty_like(h_in).pin_memory()
         for _ in range(2):
             pipe.run(h_in, h_out)
@@ -402,11 +427,11 @@ def run_ours(args):
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         (dt,) = max_over_ranks([dt], device=dev)
-        e2e = {"value": round(world * B * e_steps / dt, 3), "unit": UNIT,
+        e2e = {"value": round(world * e2e_n * e_steps / dt, 3), "unit": UNIT, "frames_per_gpu": e2e_n,
                "h2d_bytes_per_step": int(h_in.numel() * 4) * world, "d2h_bytes_per_step": int(h_out.numel() * 4) * world,
                "path": f"pinned host -> H2D -> dfc_fill_batch -> D2H, {pipe.chunk}-frame chunks on 3 streams, "
                        "wall clock"}
-        ok = bool(torch.equal(h_out, out.cpu()))
+        ok = bool(torch.equal(h_out, out[:e2e_n].cpu()))
         e2e["matches_device_path"] = ok
 
     # ---- e2e with KITTI 16-bit raw at the boundary (informational) ---------
@@ -414,7 +439,7 @@ def run_ours(args):
     if not args.no_e2e and not multi:
         from paper_1802_00036_b200 import kitti
 
-        raw_host = torch.from_numpy(np.clip(np.rint(host.astype(np.float64) * 256.0), 0, 65535)
+        raw_host = torch.from_numpy(np.clip(np.rint(host[:e2e_n].astype(np.float64) * 256.0), 0, 65535)
                                     .astype(np.uint16)).pin_memory()
         raw_out = torch.empty_like(raw_host).pin_memory()
         rpipe = kitti.RawPipeline(config, chunk=64 if W * H < 1 << 20 else 8)
@@ -430,7 +455,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         (dt,) = max_over_ranks([dt], device=dev)
-        e2e_raw16 = {"value": round(world * B * e_steps / dt, 3), "unit": UNIT,
+        e2e_raw16 = {"value": round(world * e2e_n * e_steps / dt, 3), "unit": UNIT,
                      "h2d_bytes_per_step": int(raw_host.numel() * 2) * world,
                      "d2h_bytes_per_step": int(raw_out.numel() * 2) * world,
                      "path": "pinned uint16 KITTI raw (depth * 256) -> H2D -> dfc_fill_batch_raw16 -> D2H "
@@ -440,18 +465,21 @@ def run_ours(args):
     pk, pk_src = hbm_peak()
     alg_bytes = 8 * W * H * B  # one f32 read + one f32 write per pixel
     achieved = alg_bytes / (kern_ms / 1e3) / 1e9
-    traffic = None
+    # ncu DRAM bytes per frame of this config's own capture (profiles/traffic.json,
+    # keyed by config id and path); null when the config has none
+    traffic = traffic_src = None
     tf = ROOT / "profiles" / "traffic.json"
     if tf.exists():
         try:
-            td = json.loads(tf.read_text())
-            key = "staged" if args.force_staged else "fused"
-            if key in td:
-                traffic = td[key]["dram_bytes_per_frame"] * B
+            td = json.loads(tf.read_text()).get(str(CONFIG_ID), {})
+            ent = td.get("staged" if args.force_staged else "fused")
+            if ent:
+                traffic = int(ent["dram_bytes_per_frame"] * B)
+                traffic_src = ent.get("source")
         except Exception:  # noqa: BLE001
             traffic = None
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk, "unit": "GB/s",
-            "frac": round(achieved / pk, 4), "traffic": traffic, "peak_source": pk_src,
+            "frac": round(achieved / pk, 4), "traffic": traffic, "traffic_source": traffic_src, "peak_source": pk_src,
             "algorithmic_bytes_per_launch": alg_bytes, "kernel_ms_per_launch": round(kern_ms, 4),
             "kernel": "dfc_fill_batch: every kernel of the step (r0 prologue, [multiscale stage 2], fused pipeline kernel, [blur tail], status finalize), CUDA events on its stream"}
 
@@ -465,7 +493,8 @@ def run_ours(args):
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": max(args.warmup, 3), "ms_per_step": round(ms_step, 4), "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, SURVEY 8(d))",
+                "scaling": "strong" if args.total_frames else "weak", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic (seeded, SURVEY 8(d))",
                 "config": config_block(B, args), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "e2e_raw16": e2e_raw16,
                 "clocks": clk, "gpu_launches": launches, "fallback_frames_per_step": n_fallback,
@@ -479,8 +508,13 @@ def main():
     global CONFIG_ID
     args = parse()
     CONFIG_ID = args.config
-    if args.frames is None:
-        args.frames = CONFIGS[CONFIG_ID][3]
+    if args.frames is None and args.total_frames is None:
+        if CONFIGS[CONFIG_ID][5] == "strong":
+            args.total_frames = CONFIGS[CONFIG_ID][3]
+        else:
+            args.frames = CONFIGS[CONFIG_ID][3]
+    if args.frames is None:  # reference arm / config block: this rank's share
+        args.frames = -(-args.total_frames // args.gpus)
     if args.impl == "reference":
         run_reference(args)
     else:

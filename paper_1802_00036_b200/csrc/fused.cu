@@ -22,9 +22,34 @@ namespace {
 // md - v <= 0.1, i.e. only if the frame's max already is (md - v is monotone),
 // so only such frames (count_in) are recounted here with the plain v > 0.1
 // (pipeline.py:138-141), the raw input as raw > 25 (raw / 256 > 0.1).
-__global__ void finalize_kernel(const void* __restrict__ in_v, int64_t HW, const unsigned* __restrict__ umax,
-                                uint32_t* status, float md, bool in_raw, unsigned* vcount, bool count_in) {
+// Frames whose fused output may hold an empty pixel (kRecountOut, FULL mode)
+// get their valid outputs recounted from the stored output.
+__device__ void recount_outputs(const void* out_v, int64_t HW, int64_t b, bool out_raw, unsigned* vcount) {
+  __shared__ unsigned sc;
+  if (threadIdx.x == 0) sc = 0;
+  __syncthreads();
+  unsigned n = 0;
+  if (out_raw) {
+    const uint16_t* o = static_cast<const uint16_t*>(out_v) + b * HW;
+    for (int64_t i = threadIdx.x; i < HW; i += blockDim.x) n += o[i] > 25u;  // raw / 256 > 0.1
+  } else {
+    const float* o = static_cast<const float*>(out_v) + b * HW;
+    for (int64_t i = threadIdx.x; i < HW; i += blockDim.x) n += o[i] > kValid;
+  }
+  n = __reduce_add_sync(kFull, n);
+  if ((threadIdx.x & 31) == 0 && n) atomicAdd(&sc, n);
+  __syncthreads();
+  if (threadIdx.x == 0) vcount[2 * b + 1] = sc;
+}
+
+__global__ void finalize_kernel(const void* __restrict__ in_v, const void* __restrict__ out_v, int64_t HW,
+                                const unsigned* __restrict__ umax, uint32_t* status, float md, bool in_raw,
+                                bool out_raw, unsigned* vcount, bool count_in) {
   const int64_t b = blockIdx.x;
+  if (status[b] & kRecountOut) {  // uniform: every thread reads it before anyone clears it
+    recount_outputs(out_v, HW, b, out_raw, vcount);
+    if (threadIdx.x == 0) atomicAnd(status + b, ~kRecountOut);
+  }
   const unsigned u = umax[b];
   const float uf = __uint_as_float(u);
   const bool rare = count_in && uf > kValid && uf < md && !(__fadd_rn(md, -uf) > kValid);
@@ -283,7 +308,8 @@ cudaError_t launch_fused(const void* in_v, void* out_v, int64_t B, int H, int W,
       return e;
   }
   note_launch();
-  finalize_kernel<<<(unsigned)B, 256, 0, s>>>(in_v, HW, umax0, status, c.max_depth, io != 0, vcount, !pre);
+  finalize_kernel<<<(unsigned)B, 256, 0, s>>>(in_v, out_v, HW, umax0, status, c.max_depth, io != 0, io == 2, vcount,
+                                              !pre);
   return cudaGetLastError();
 }
 

@@ -71,6 +71,7 @@ constexpr int kMbCount = 32;            // mbarrier arrivals per phase: every la
 constexpr int kLF = 15;                // large fill radius
 constexpr int kStripMax = 1248;        // widest strip handled by one CTA
 constexpr uint32_t kNeedsStaged = 0x200u;  // internal status bit (capi.cu)
+constexpr uint32_t kRecountOut = 0x400u;   // internal: finalize_kernel recounts the frame's valid outputs
 constexpr int kBlurRaw = -1;           // emit the stage-6 (FULL) / stage-4 (PARTIAL) inverted map for blur_tail.cu
 constexpr int64_t kRawChunk = 296;     // frames per fused -> blur-tail round (2 per SM) in the raw mode
 
@@ -215,6 +216,20 @@ __device__ __forceinline__ void store_lane_t(T* q, const F4& a, unsigned colmask
 __device__ __forceinline__ unsigned valid_mask(const F4& a) {
   return (unsigned)(a.v[0] > kValid) | (unsigned)(a.v[1] > kValid) << 1 | (unsigned)(a.v[2] > kValid) << 2 |
          (unsigned)(a.v[3] > kValid) << 3;
+}
+
+// store_lane_t plus the min over the stored values (FULL output check, S.omin):
+// the full-lane branch takes the min of all four, the partial one per column
+template <int VEC, typename T>
+__device__ __forceinline__ void store_lane_min(T* q, const F4& a, unsigned colmask, bool& over, float& omin) {
+  if (colmask == 0xFu) {
+    omin = fmn3(fmn3(omin, a.v[0], a.v[1]), a.v[2], a.v[3]);
+  } else {
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (colmask >> c & 1u) omin = fminf(omin, a.v[c]);
+  }
+  store_lane_t<VEC>(q, a, colmask, over);
 }
 
 // ---------------------------------------------------------------------------
@@ -645,12 +660,14 @@ struct State {
   bool enc_over;       // IO 2: an output >= 256 m (not encodable)
   bool full;           // all 4 columns inside the frame
   unsigned incol;
-  float amin;          // FULL: min blurred value (<= 0.1 sends the frame to the staged path)
 #ifdef DFC_TIMING
   long long tacc[6];   // diagnostics: producer, barrier, consumer, phase 1, consumer LF part, store-only rows
 #endif
   unsigned umax;
-  unsigned nin, nout;  // valid-pixel counters (owned output columns): inputs read, outputs stored
+  unsigned nin, nout, outm16;  // outm16: outm in each of the four row nibbles  // valid-pixel counters (owned output columns): inputs read, outputs stored (PARTIAL)
+  float omin;          // FULL: min stored output (fast rows repeat a stored row); outputs are valid
+                       // (nearly) always, so the count is H x owned columns unless omin <= 0.1, when
+                       // finalize_kernel recounts the frame
   bool had_empty, still_empty;
   uint32_t mbW, mbL, mbR;  // shared addresses of this warp's / the neighbours' P[4], C[4] mbarriers
   bool hasL, hasR;
@@ -678,6 +695,7 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
   F4 f[kB];
   if (!S.skip) {
     F4 a[kB];
+    unsigned bm = 0;  // bit 4j + c: input row j, column c is valid
     cp_async_wait_all();  // this block's rows, staged one block ago
 #pragma unroll
     for (int j = 0; j < kB; ++j) {
@@ -688,16 +706,21 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
         S.umax = max(max(S.umax, __float_as_uint(a[j].v[2])), __float_as_uint(a[j].v[3]));
         const float2 d01 = __ffma2_rn(make_float2(a[j].v[0], a[j].v[1]), make_float2(-1.f, -1.f), make_float2(p.md, p.md));
         const float2 d23 = __ffma2_rn(make_float2(a[j].v[2], a[j].v[3]), make_float2(-1.f, -1.f), make_float2(p.md, p.md));
-        a[j].v[0] = a[j].v[0] > kValid ? d01.x : 0.0f;
-        a[j].v[1] = a[j].v[1] > kValid ? d01.y : 0.0f;
-        a[j].v[2] = a[j].v[2] > kValid ? d23.x : 0.0f;
-        a[j].v[3] = a[j].v[3] > kValid ? d23.y : 0.0f;
-        // RunStats.input_density (pipeline.py:138-141): inverted-valid inputs of the
-        // owned output columns; each row is read once (rows outside the frame are 0)
-        S.nin += __popc(((unsigned)(a[j].v[0] > kValid) | (unsigned)(a[j].v[1] > kValid) << 1 |
-                         (unsigned)(a[j].v[2] > kValid) << 2 | (unsigned)(a[j].v[3] > kValid) << 3) & S.outm);
+        const bool q0 = a[j].v[0] > kValid, q1 = a[j].v[1] > kValid;
+        const bool q2 = a[j].v[2] > kValid, q3 = a[j].v[3] > kValid;
+        a[j].v[0] = q0 ? d01.x : 0.0f;
+        a[j].v[1] = q1 ? d01.y : 0.0f;
+        a[j].v[2] = q2 ? d23.x : 0.0f;
+        a[j].v[3] = q3 ? d23.y : 0.0f;
+        // RunStats.input_density (pipeline.py:138-141): valid inputs of the owned
+        // output columns, each row read once (rows outside the frame are 0).  Rows
+        // above the skip point are not read here; they hold no input that is still
+        // valid once inverted, and finalize_kernel recounts the rare frames that
+        // hold inputs within 0.1 of max_depth.
+        bm |= ((unsigned)q0 | (unsigned)q1 << 1 | (unsigned)q2 << 2 | (unsigned)q3 << 3) << (4 * j);
       }
     }
+    if constexpr (!PRE) S.nin += __popc(bm & S.outm16);
     // stage the next block; stops once its stage-5 rows lie above every r0.
     // The values read above are materialised first: the shared reads are
     // complete before the slot is overwritten.
@@ -878,12 +901,14 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
 #endif
     // every row of the blur windows lies above each needed column's r0: the
     // stage-6 rows are the captured top values and every output row is equal
+    // output rows: tc0 - 2 + j with the Gaussian, tc0 + j otherwise (as below)
+    constexpr int kOff = BLUR == DFC_BLUR_GAUSSIAN ? 2 : 0;
+    if (kOff == 0) orow -= 2 * W;
 #pragma unroll
     for (int j = 0; j < kB; ++j, orow -= W) {
-      const int t = tc0 - 2 + j;
+      const int t = tc0 - kOff + j;
       if (EDGE && (t < 0 || t >= H)) continue;
       if (S.outm) store_lane_t<VEC>(orow, S.ofast, S.outm, S.enc_over);
-      if (BLUR != kBlurRaw) S.nout += __popc(valid_mask(S.ofast) & S.outm);
     }
     break;
   }
@@ -1065,8 +1090,12 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
         if (!FULL && !(mk[j].v[c] > kValid)) o.v[c] = 0.0f;
         if (!FULL && !(mk[j].v[c + 1] > kValid)) o.v[c + 1] = 0.0f;
       }
-      if (S.outm) store_lane_t<VEC>(orow, o, S.outm, S.enc_over);
-      S.nout += __popc(valid_mask(o) & S.outm);
+      if (FULL) {
+        if (S.outm) store_lane_min<VEC>(orow, o, S.outm, S.enc_over, S.omin);
+      } else {
+        if (S.outm) store_lane_t<VEC>(orow, o, S.outm, S.enc_over);
+        S.nout += __popc(valid_mask(o) & S.outm);
+      }
     }
     // rows tc0-4 .. tc0+3 above every needed r0: output row tc0+1 repeats from here on
     if (FULL && !EDGE && tc0 - 4 > S.tmaxN) {
@@ -1083,8 +1112,12 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
 #pragma unroll
       for (int c = 0; c < 4; ++c)
         o.v[c] = BLUR == kBlurRaw ? v6[j].v[c] : (v6[j].v[c] > kValid ? p.md - v6[j].v[c] : 0.0f);
-      if (S.outm) store_lane_t<VEC>(orow, o, S.outm, S.enc_over);
-      if (BLUR != kBlurRaw) S.nout += __popc(valid_mask(o) & S.outm);
+      if (FULL && BLUR != kBlurRaw) {
+        if (S.outm) store_lane_min<VEC>(orow, o, S.outm, S.enc_over, S.omin);
+      } else {
+        if (S.outm) store_lane_t<VEC>(orow, o, S.outm, S.enc_over);
+        if (BLUR != kBlurRaw) S.nout += __popc(valid_mask(o) & S.outm);
+      }
     }
     if (FULL && !EDGE && tc0 > S.tmaxN) {
       S.fast = true;
@@ -1172,6 +1205,8 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
     S.compR = (S.x0 <= W - 1 && W - 1 <= S.x0 + 3) ? W - 1 - S.x0 : -1;  // component of column W - 1
     S.umax = 0;
     S.nin = S.nout = 0;
+    S.outm16 = S.outm * 0x1111u;
+    S.omin = kFMax;
     S.had_empty = S.still_empty = false;
     S.skip = S.fast = S.enc_over = false;
     S.mbW = mb0 + warp * 64;
@@ -1263,7 +1298,11 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
     gk = S.gk;
     // ---------------- per-frame flags ----------------
     const unsigned um = __reduce_max_sync(kFull, S.umax);
-    const unsigned nin = __reduce_add_sync(kFull, S.nin), nout = __reduce_add_sync(kFull, S.nout);
+    const unsigned nin = __reduce_add_sync(kFull, S.nin);
+    const unsigned nout = FULL ? __reduce_add_sync(kFull, (unsigned)__popc(S.outm)) * (unsigned)H
+                               : __reduce_add_sync(kFull, S.nout);
+    const bool recount = FULL && BLUR != kBlurRaw && !(__uint_as_float(__reduce_min_sync(kFull,
+                                                                      __float_as_uint(S.omin))) > kValid);
     const bool he = __any_sync(kFull, S.had_empty);
     const bool se = __any_sync(kFull, S.still_empty);
     const bool eo = IO == 2 && __any_sync(kFull, S.enc_over);
@@ -1271,6 +1310,7 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
       if (!PRE) atomicMax(p.umax + frame, um);  // PRE: multiscale.cu records it
       if (!PRE && nin) atomicAdd(p.vcount + 2 * frame, nin);  // PRE: multiscale.cu counts the inputs
       if (BLUR != kBlurRaw && nout) atomicAdd(p.vcount + 2 * frame + 1, nout);  // raw: the blur tail counts
+      if (recount) atomicOr(p.status + frame, kRecountOut);
       if (eo) atomicOr(p.status + frame, DFC_ST_ENCODE);
       if (FULL && he && p.iters) atomicOr(p.iters + frame, 1);
       if (FULL && se) {

@@ -632,11 +632,21 @@ __device__ __forceinline__ void mb_arrive(uint32_t a) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(a) : "memory");
 }
 __device__ __forceinline__ void mb_wait(uint32_t a, uint32_t parity) {
+#ifdef DFC_MB_HINT
+  // suspend until the phase completes (or the hint, in ns, elapses) instead of
+  // re-polling: the spin loop's YIELD / TRYWAIT / BRA took issue slots
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1, %2;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(a),
+      "r"(parity), "n"(DFC_MB_HINT)
+      : "memory");
+#else
   asm volatile(
       "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
       " @!p bra WAIT_%=;\n}\n" ::"r"(a),
       "r"(parity)
       : "memory");
+#endif
 }
 
 struct State {
@@ -664,7 +674,8 @@ struct State {
   long long tacc[6];   // diagnostics: producer, barrier, consumer, phase 1, consumer LF part, store-only rows
 #endif
   unsigned umax;
-  unsigned nin, nout, outm16;  // outm16: outm in each of the four row nibbles  // valid-pixel counters (owned output columns): inputs read, outputs stored (PARTIAL)
+  float2 cin01, cin23, own01, own23;  // per-column valid-input counts (float, exact < 2^24), owned-column weights
+  unsigned nin, nout;  // valid-pixel counters (owned output columns): inputs read, outputs stored (PARTIAL)
   float omin;          // FULL: min stored output (fast rows repeat a stored row); outputs are valid
                        // (nearly) always, so the count is H x owned columns unless omin <= 0.1, when
                        // finalize_kernel recounts the frame
@@ -695,7 +706,6 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
   F4 f[kB];
   if (!S.skip) {
     F4 a[kB];
-    unsigned bm = 0;  // bit 4j + c: input row j, column c is valid
     cp_async_wait_all();  // this block's rows, staged one block ago
 #pragma unroll
     for (int j = 0; j < kB; ++j) {
@@ -706,21 +716,23 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
         S.umax = max(max(S.umax, __float_as_uint(a[j].v[2])), __float_as_uint(a[j].v[3]));
         const float2 d01 = __ffma2_rn(make_float2(a[j].v[0], a[j].v[1]), make_float2(-1.f, -1.f), make_float2(p.md, p.md));
         const float2 d23 = __ffma2_rn(make_float2(a[j].v[2], a[j].v[3]), make_float2(-1.f, -1.f), make_float2(p.md, p.md));
-        const bool q0 = a[j].v[0] > kValid, q1 = a[j].v[1] > kValid;
-        const bool q2 = a[j].v[2] > kValid, q3 = a[j].v[3] > kValid;
-        a[j].v[0] = q0 ? d01.x : 0.0f;
-        a[j].v[1] = q1 ? d01.y : 0.0f;
-        a[j].v[2] = q2 ? d23.x : 0.0f;
-        a[j].v[3] = q3 ? d23.y : 0.0f;
-        // RunStats.input_density (pipeline.py:138-141): valid inputs of the owned
-        // output columns, each row read once (rows outside the frame are 0).  Rows
-        // above the skip point are not read here; they hold no input that is still
-        // valid once inverted, and finalize_kernel recounts the rare frames that
-        // hold inputs within 0.1 of max_depth.
-        bm |= ((unsigned)q0 | (unsigned)q1 << 1 | (unsigned)q2 << 2 | (unsigned)q3 << 3) << (4 * j);
+        // validity as 1.0f / 0.0f (one FSET each, ALU pipe); the select and the
+        // RunStats.input_density count (pipeline.py:138-141) then run on the FMA
+        // pipe: (md - v) * 1 and (md - v) * 0 are exact (md - v > 0 on frames
+        // that do not raise), and the per-lane count weights each column by
+        // whether this lane owns it as an output column.  Rows above the skip
+        // point are not read here; they hold no input that is still valid once
+        // inverted, and finalize_kernel recounts the rare frames that hold
+        // inputs within 0.1 of max_depth.
+        const float2 q01 = make_float2(a[j].v[0] > kValid ? 1.f : 0.f, a[j].v[1] > kValid ? 1.f : 0.f);
+        const float2 q23 = make_float2(a[j].v[2] > kValid ? 1.f : 0.f, a[j].v[3] > kValid ? 1.f : 0.f);
+        const float2 m01 = __fmul2_rn(d01, q01), m23 = __fmul2_rn(d23, q23);
+        a[j].v[0] = m01.x, a[j].v[1] = m01.y, a[j].v[2] = m23.x, a[j].v[3] = m23.y;
+        S.cin01 = __ffma2_rn(q01, S.own01, S.cin01);
+        S.cin23 = __ffma2_rn(q23, S.own23, S.cin23);
       }
     }
-    if constexpr (!PRE) S.nin += __popc(bm & S.outm16);
+
     // stage the next block; stops once its stage-5 rows lie above every r0.
     // The values read above are materialised first: the shared reads are
     // complete before the slot is overwritten.
@@ -1085,8 +1097,10 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
         for (int i = 1; i < 5; ++i)
           a = __ffma2_rn(make_float2(in[j + i].v[c], in[j + i].v[c + 1]), make_float2(p.gw[i], p.gw[i]), a);
         const float2 r = __ffma2_rn(a, make_float2(-1.f, -1.f), make_float2(p.md, p.md));  // md - a, exact negation
-        o.v[c] = a.x > kValid ? r.x : 0.0f;
-        o.v[c + 1] = a.y > kValid ? r.y : 0.0f;
+        // invert back (depth_core.py:150-156): (md - a) * 1.0f / 0.0f; md - a > 0 (a < md)
+        const float2 ov = __fmul2_rn(r, make_float2(a.x > kValid ? 1.f : 0.f, a.y > kValid ? 1.f : 0.f));
+        o.v[c] = ov.x;
+        o.v[c + 1] = ov.y;
         if (!FULL && !(mk[j].v[c] > kValid)) o.v[c] = 0.0f;
         if (!FULL && !(mk[j].v[c + 1] > kValid)) o.v[c + 1] = 0.0f;
       }
@@ -1205,7 +1219,9 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
     S.compR = (S.x0 <= W - 1 && W - 1 <= S.x0 + 3) ? W - 1 - S.x0 : -1;  // component of column W - 1
     S.umax = 0;
     S.nin = S.nout = 0;
-    S.outm16 = S.outm * 0x1111u;
+    S.cin01 = S.cin23 = make_float2(0.f, 0.f);
+    S.own01 = make_float2((float)(S.outm & 1u), (float)(S.outm >> 1 & 1u));
+    S.own23 = make_float2((float)(S.outm >> 2 & 1u), (float)(S.outm >> 3 & 1u));
     S.omin = kFMax;
     S.had_empty = S.still_empty = false;
     S.skip = S.fast = S.enc_over = false;
@@ -1298,6 +1314,7 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
     gk = S.gk;
     // ---------------- per-frame flags ----------------
     const unsigned um = __reduce_max_sync(kFull, S.umax);
+    S.nin = (unsigned)(S.cin01.x + S.cin01.y + S.cin23.x + S.cin23.y);
     const unsigned nin = __reduce_add_sync(kFull, S.nin);
     const unsigned nout = FULL ? __reduce_add_sync(kFull, (unsigned)__popc(S.outm)) * (unsigned)H
                                : __reduce_add_sync(kFull, S.nout);

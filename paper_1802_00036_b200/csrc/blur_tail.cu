@@ -37,12 +37,17 @@ namespace {
 constexpr int kMW = 64, kMH = 64, kThreads = 256;
 static_assert((kMW / kMedBlockW) * (kMH / kMedBlockH) == kThreads, "one median block per thread");
 constexpr int kPostNone = 0, kPostGauss = 1, kPostBilateral = 2;
+constexpr unsigned kFullMask = 0xffffffffu;
+#ifndef DFC_TAIL_MINB
+#define DFC_TAIL_MINB 3  // resident CTAs per SM the register allocation targets (<= 80 registers)
+#endif
 
 struct TailParams {
   float md;
   float w2[25];  // Gaussian 2-D taps w_i * w_j (row-major, radius PR)
   float ks[25];  // bilateral: log2(e) * spatial exponent per tap (dy^2 + dx^2) / (-2 sigma_s^2)
   float kv;      // bilateral: log2(e) / (-2 sigma_v^2)
+  float bsc, bisc;  // bilateral: sqrt(-kv) and its inverse (bilateral5_sym prescales the values)
   unsigned* vcount;  // [B][2] (may be null): [1] += valid outputs (RunStats.output_density)
 };
 
@@ -53,6 +58,12 @@ struct TailParams {
     a = lo_;                       \
     b = hi_;                       \
   } while (0)
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 __device__ __forceinline__ float ex2_ftz(float x) {
   float y;
@@ -91,10 +102,10 @@ struct TileGeo {
   // shared row stride: odd, so the 8x2 median blocks of a warp (bases 8 bx +
   // 2 IWS by) fall on 16 distinct banks instead of 4 (2-way, not 8-way,
   // conflicts; config 2: 110k -> 114.5k frames/s)
-  static constexpr int IWS = IW | 1;
-  // Double-buffered persistent CTAs only with the median (long ALU phase to
-  // hide the next tile's staging behind); without it, one tile per CTA and
-  // more resident CTAs hide the loads better (config 0).
+  static constexpr int IWS = MR > 0 ? (IW | 1) : IW;  // MR = 0: 8-byte aligned rows (bilateral5_sym reads sIn)
+  // Double-buffered persistent CTAs with the median or the 5x5 bilateral (long
+  // ALU phases, few resident CTAs: the next tile's staging hides behind them);
+  // otherwise one tile per CTA and more resident CTAs hide the loads better.
   static constexpr bool kDB = MR > 0;
   static constexpr size_t kSmem = (size_t)(2 * IH * IWS + kMW * kMH) * sizeof(float);
 };
@@ -109,9 +120,9 @@ template <int MR, int PR>
 __device__ __forceinline__ void stage_tile(const float* __restrict__ in, int H, int W, int tx, int ty, int64_t t,
                                            float* sIn) {
   using G = TileGeo<MR, PR>;
-  const int64_t b = t / ((int64_t)tx * ty);
-  const int r = (int)(t - b * tx * ty), byi = r / tx, bxi = r - byi * tx;
-  const int x0 = bxi * G::TX, y0 = byi * G::TY;
+  const unsigned per = (unsigned)(tx * ty), tu = (unsigned)t;  // tiles < 2^31 (launch_t chunks the batch)
+  const unsigned b = tu / per, r = tu - b * per, byi = r / (unsigned)tx, bxi = r - byi * (unsigned)tx;
+  const int x0 = (int)bxi * G::TX, y0 = (int)byi * G::TY;
   const float* src = in + b * (int64_t)H * W;
   const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(sIn);
   if (x0 - G::HI >= 0 && y0 - G::HI >= 0 && x0 - G::HI + G::IW <= W && y0 - G::HI + G::IH <= H) {
@@ -142,6 +153,188 @@ __device__ __forceinline__ void stage_tile(const float* __restrict__ in, int H, 
   }
 }
 
+// Stage 7c (re-impose) + stage 8 for one output pair and its store:
+// PARTIAL keeps the pre-blur validity (pipeline.py:212-214), then invert back
+// (depth_core.py:150-156).
+template <bool PARTIAL, bool OUT16, bool BLUR>
+__device__ __forceinline__ void finish_pair(float2 r, float2 c, void* __restrict__ out_v, int64_t off, int gx, int W,
+                                            const TailParams& p, bool& over, unsigned& nvalid) {
+  float o[2] = {r.x, r.y};
+  const float cc[2] = {c.x, c.y};
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    if (PARTIAL && BLUR && !(cc[h] > kValid)) o[h] = 0.0f;
+    o[h] = o[h] > kValid ? p.md - o[h] : 0.0f;
+  }
+  nvalid += (o[0] > kValid) + (gx + 1 < W && o[1] > kValid);
+  if constexpr (OUT16) {
+    uint16_t* q = static_cast<uint16_t*>(out_v) + off;
+    over |= o[0] >= 256.0f || (gx + 1 < W && o[1] >= 256.0f);
+    if (gx + 1 < W && (reinterpret_cast<uintptr_t>(q) & 3) == 0)
+      __stcs(reinterpret_cast<unsigned*>(q), enc_raw16(o[0]) | enc_raw16(o[1]) << 16);
+    else {
+      q[0] = (uint16_t)enc_raw16(o[0]);
+      if (gx + 1 < W) q[1] = (uint16_t)enc_raw16(o[1]);
+    }
+  } else {
+    float* q = static_cast<float*>(out_v) + off;
+    if (gx + 1 < W) {
+      if ((reinterpret_cast<uintptr_t>(q) & 7) == 0)
+        __stcs(reinterpret_cast<float2*>(q), make_float2(o[0], o[1]));
+      else
+        __stcs(q, o[0]), __stcs(q + 1, o[1]);
+    } else {
+      __stcs(q, o[0]);
+    }
+  }
+}
+
+// 5x5 bilateral (morphology.py:115-125, _numpy_ops.py:76-95) with the weights
+// shared between the two pixels of every pair: w(p, p+d) = ex2(ks(d) - (sc
+// (v(p+d) - v(p)))^2) is symmetric (ks(-d) = ks(d); float a - b = -(b - a)
+// exactly, so both directions round identically), so each pixel evaluates the
+// 12 forward offsets d (dy > 0, or dy = 0 and dx > 0) only: 12 ex2 per output
+// instead of 24 (the MUFU pipe bounded this kernel).  Each weight adds w (q - p)
+// to p's sums and is pushed, as -w (q - p), to the pixel q = p + d: into the
+// pending sums of the row dy below (registers), through a shuffle when q lies
+// in the neighbour lane.  Warp w sweeps a band of 8 output rows top-down over
+// the whole 64-column region (lane l holds sM columns 2l, 2l+1 = output columns
+// 2l-2, 2l-1; lanes 1..30 own outputs, lanes 0 / 31 evaluate the weights
+// their neighbours take), starting with two warm-up rows that push only.
+// Values are prescaled by sc = sqrt(-kv) (kv = log2(e) / (-2 sigma_v^2)), so
+// the exponent is one FFMA2: ks - d'^2 with d' = sc d (prescaled differences
+// round differently from d: ~1e-6 m at most in the output, the bar is 1e-4).
+// fp32 centre-relative: out = c + sum w d / (1 + sum w).
+template <bool PARTIAL, bool OUT16, int MW>
+__device__ __forceinline__ void bilateral5_sym(const float* __restrict__ sM, void* __restrict__ out_v, int H, int W,
+                                               const TailParams& p, int64_t b, int x0, int y0, bool& over,
+                                               unsigned& nvalid) {
+  constexpr int TY = kMH - 4, NW = kThreads / 32;
+  constexpr int kBand = (TY + NW - 1) / NW;  // 8 output rows per warp (bands overlap by <= 1 row)
+  static_assert(MW % 2 == 0, "float2 rows");
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // every warp sweeps exactly kBand rows (straight-line code: the shuffles need
+  // no reconvergence); it stores only the rows below the next band's start
+  const int ra = warp * (TY - kBand) / (NW - 1), rb = warp == NW - 1 ? TY : (warp + 1) * (TY - kBand) / (NW - 1);
+  const int X0 = 2 * lane;
+  // the first / last lane's outer columns are never used: clamp their loads into the region
+  const int cA = max(X0 - 2, 0), cC = min(X0 + 2, kMW - 2);
+  const float2 sc = make_float2(p.bsc, p.bsc);
+  const int gx = x0 + X0 - 2;       // output column of the pair
+  const bool Weven = (W & 1) == 0;  // gx is even: float2 stores are aligned
+  const int64_t obase = b * (int64_t)H * W + (int64_t)y0 * W + gx;
+  float* const fbase = static_cast<float*>(out_v) + b * (int64_t)H * W;
+  int ooff = (y0 + ra) * W + gx;  // 32-bit in-frame offset of the output pair of sweep step i >= 2 (H W < 2^31)
+  // V[r][k]: prescaled sM row s + r, column X0 - 2 + k; C[r]: the unscaled centre pair of that row
+  float V[3][6];
+  float2 C[3];
+  auto load_row = [&](int s, float* v, float2& c) {
+    const float* r = sM + s * MW;
+    const float2 a = *reinterpret_cast<const float2*>(r + cA);
+    const float2 m = *reinterpret_cast<const float2*>(r + X0);
+    const float2 e = *reinterpret_cast<const float2*>(r + cC);
+    c = m;
+    const float2 a2 = __fmul2_rn(a, sc), m2 = __fmul2_rn(m, sc), e2 = __fmul2_rn(e, sc);
+    v[0] = a2.x, v[1] = a2.y, v[2] = m2.x, v[3] = m2.y, v[4] = e2.x, v[5] = e2.y;
+  };
+  // pending (acc, den) pushed to rows s, s + 1, s + 2
+  float2 Qa[3], Qd[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) Qa[k] = Qd[k] = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int r = 0; r < 3; ++r) load_row(ra + r, V[r], C[r]);
+#pragma unroll
+  for (int i = 0; i < kBand + 2; ++i) {
+    const int s = ra + i;  // sM row (output row s - 2)
+    if (i > 0) {
+#pragma unroll
+      for (int k = 0; k < 6; ++k) V[0][k] = V[1][k], V[1][k] = V[2][k];
+      C[0] = C[1], C[1] = C[2];
+      load_row(s + 2, V[2], C[2]);
+    }
+    const bool outrow = i >= 2;
+    float2 Fa = make_float2(0.f, 0.f), Fd = make_float2(0.f, 0.f);  // forward sums of this row's pixels
+    const float2 c2 = make_float2(V[0][2], V[0][3]);
+#pragma unroll
+    for (int dy = 0; dy < 3; ++dy) {
+      // warm-up rows push only what reaches the band: row ra - 2 (i = 0) the dy = 2
+      // offsets, row ra - 1 (i = 1) dy >= 1; dy = 0 only on output rows
+      if ((i == 0 && dy < 2) || (i == 1 && dy < 1)) continue;
+      float2 La = make_float2(0.f, 0.f), Ld = La, Ra = La, Rd = La;  // pushes to the left / right lane
+      bool hasL = false;
+#pragma unroll
+      for (int dx = -2; dx <= 2; ++dx) {
+        if (dy == 0 && dx <= 0) continue;
+        const float ks = p.ks[(dy + 2) * 5 + dx + 2];
+        const float2 n = make_float2(V[dy][2 + dx], V[dy][3 + dx]);
+        const float2 d = __fadd2_rn(n, make_float2(-c2.x, -c2.y));
+        const float2 e = __ffma2_rn(make_float2(-d.x, -d.y), d, make_float2(ks, ks));  // exponents <= 0
+        const float2 w = make_float2(ex2_ftz(e.x), ex2_ftz(e.y));
+        const float2 wd = __fmul2_rn(w, d);
+        if (outrow) {
+          Fa = __fadd2_rn(Fa, wd);
+          Fd = __fadd2_rn(Fd, w);
+        }
+        // push -w d and w to q = p + (dy, dx): lane offset / component by (comp + dx)
+        if (dx == 0) {
+          Qa[dy] = __fadd2_rn(Qa[dy], make_float2(-wd.x, -wd.y));
+          Qd[dy] = __fadd2_rn(Qd[dy], w);
+        } else if (dx == -2) {
+          La = make_float2(-wd.x, -wd.y), Ld = w, hasL = true;
+        } else if (dx == 2) {
+          Ra = __fadd2_rn(Ra, make_float2(-wd.x, -wd.y));
+          Rd = __fadd2_rn(Rd, w);
+        } else if (dx == -1) {  // x -> left lane's y; y -> own x
+          La.y -= wd.x, Ld.y += w.x;
+          Qa[dy].x -= wd.y, Qd[dy].x += w.y;
+          hasL = true;
+        } else {  // dx == 1: x -> own y; y -> right lane's x
+          Qa[dy].y -= wd.x, Qd[dy].y += w.x;
+          Ra.x -= wd.y, Rd.x += w.y;
+        }
+      }
+      // receive: the right lane's left pushes and the left lane's right pushes
+      if (hasL) {
+        const float2 ra_ = make_float2(__shfl_down_sync(kFullMask, La.x, 1), __shfl_down_sync(kFullMask, La.y, 1));
+        const float2 rd_ = make_float2(__shfl_down_sync(kFullMask, Ld.x, 1), __shfl_down_sync(kFullMask, Ld.y, 1));
+        Qa[dy] = __fadd2_rn(Qa[dy], ra_);
+        Qd[dy] = __fadd2_rn(Qd[dy], rd_);
+      }
+      {
+        const float2 ra_ = make_float2(__shfl_up_sync(kFullMask, Ra.x, 1), __shfl_up_sync(kFullMask, Ra.y, 1));
+        const float2 rd_ = make_float2(__shfl_up_sync(kFullMask, Rd.x, 1), __shfl_up_sync(kFullMask, Rd.y, 1));
+        Qa[dy] = __fadd2_rn(Qa[dy], ra_);
+        Qd[dy] = __fadd2_rn(Qd[dy], rd_);
+      }
+    }
+    if (outrow) {
+      const float2 acc = __fadd2_rn(Qa[0], Fa);
+      const float2 den = __fadd2_rn(__fadd2_rn(Qd[0], Fd), make_float2(1.f, 1.f));  // centre tap: weight 1
+      // den >= 1: rcp.approx.ftz needs no denormal handling; acc is in prescaled units
+      const float2 q = __fmul2_rn(make_float2(rcp_approx(den.x), rcp_approx(den.y)), make_float2(p.bisc, p.bisc));
+      const float2 c = C[0];
+      const float2 r = __ffma2_rn(acc, q, c);
+      const int oy = s - 2;
+      if (lane != 0 && lane != 31 && oy < rb && y0 + oy < H && gx < W) {
+        if (!OUT16 && Weven && gx + 1 < W) {
+          // the common case: [re-impose,] invert back and one aligned 8-byte store
+          float o0 = r.x > kValid ? p.md - r.x : 0.0f, o1 = r.y > kValid ? p.md - r.y : 0.0f;
+          if (PARTIAL && !(c.x > kValid)) o0 = 0.0f;
+          if (PARTIAL && !(c.y > kValid)) o1 = 0.0f;
+          nvalid += (o0 > kValid) + (o1 > kValid);
+          __stcs(reinterpret_cast<float2*>(fbase + ooff), make_float2(o0, o1));
+        } else {
+          finish_pair<PARTIAL, OUT16, true>(r, c, out_v, obase + (int64_t)oy * W, gx, W, p, over, nvalid);
+        }
+      }
+      ooff += W;
+    }
+    Qa[0] = Qa[1], Qd[0] = Qd[1];
+    Qa[1] = Qa[2], Qd[1] = Qd[2];
+    Qa[2] = Qd[2] = make_float2(0.f, 0.f);
+  }
+}
+
 // One output tile from its staged input: median -> blur -> re-impose -> invert back -> store.
 template <int MR, int POST, int PR, bool PARTIAL, bool OUT16>
 __device__ __forceinline__ void tile_process(const float* __restrict__ sIn, float* __restrict__ sM,
@@ -153,6 +346,17 @@ __device__ __forceinline__ void tile_process(const float* __restrict__ sIn, floa
   bool over = false;  // OUT16: an output >= 256 m
   unsigned nvalid = 0;
 
+  if constexpr (MR == 0 && POST == kPostBilateral && PR == 2) {
+    // no median: the staged tile (frame-clamped positions = replicate border)
+    // is the blur input as it is
+    bilateral5_sym<PARTIAL, OUT16, IWS>(sIn, out_v, H, W, p, b, x0, y0, over, nvalid);
+    if (OUT16 && over) atomicOr(status + b, DFC_ST_ENCODE);
+    if (p.vcount) {
+      nvalid = __reduce_add_sync(0xffffffffu, nvalid);
+      if ((threadIdx.x & 31) == 0 && nvalid) atomicAdd(p.vcount + 2 * b + 1, nvalid);
+    }
+    return;
+  }
   // stage-7a: median (or copy) on the tile + blur halo, at frame-clamped centres
   if constexpr (MR == 2) {
     // shared 8x2-block network on the regular grid; positions outside the
@@ -198,6 +402,9 @@ __device__ __forceinline__ void tile_process(const float* __restrict__ sIn, floa
 
   // stage-7b: Gaussian / bilateral, re-impose, invert back -- two horizontally
   // adjacent outputs per thread in packed fp32x2 (FADD2 / FMUL2 / FFMA2)
+  if constexpr (POST == kPostBilateral && PR == 2) {
+    bilateral5_sym<PARTIAL, OUT16, MW>(sM, out_v, H, W, p, b, x0, y0, over, nvalid);
+  } else
   for (int i = threadIdx.x; i < kTX * kTY / 2; i += kThreads) {
     const int oy = i / (kTX / 2), ox = 2 * (i - oy * (kTX / 2));
     const int gy = y0 + oy, gx = x0 + ox;
@@ -245,35 +452,8 @@ __device__ __forceinline__ void tile_process(const float* __restrict__ sIn, floa
         }
       r = make_float2(c.x + __fdividef(acc.x, den.x), c.y + __fdividef(acc.y, den.y));
     }
-    float o[2] = {r.x, r.y};
-    const float cc[2] = {c.x, c.y};
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      if (PARTIAL && POST != kPostNone && !(cc[h] > kValid)) o[h] = 0.0f;
-      o[h] = o[h] > kValid ? p.md - o[h] : 0.0f;
-    }
-    nvalid += (o[0] > kValid) + (gx + 1 < W && o[1] > kValid);
-    const int64_t off = b * (int64_t)H * W + (int64_t)gy * W + gx;
-    if constexpr (OUT16) {
-      uint16_t* q = static_cast<uint16_t*>(out_v) + off;
-      over |= o[0] >= 256.0f || (gx + 1 < W && o[1] >= 256.0f);
-      if (gx + 1 < W && (reinterpret_cast<uintptr_t>(q) & 3) == 0)
-        __stcs(reinterpret_cast<unsigned*>(q), enc_raw16(o[0]) | enc_raw16(o[1]) << 16);
-      else {
-        q[0] = (uint16_t)enc_raw16(o[0]);
-        if (gx + 1 < W) q[1] = (uint16_t)enc_raw16(o[1]);
-      }
-    } else {
-      float* q = static_cast<float*>(out_v) + off;
-      if (gx + 1 < W) {
-        if ((reinterpret_cast<uintptr_t>(q) & 7) == 0)
-          __stcs(reinterpret_cast<float2*>(q), make_float2(o[0], o[1]));
-        else
-          __stcs(q, o[0]), __stcs(q + 1, o[1]);
-      } else {
-        __stcs(q, o[0]);
-      }
-    }
+    finish_pair<PARTIAL, OUT16, POST != kPostNone>(r, c, out_v, b * (int64_t)H * W + (int64_t)gy * W + gx, gx, W, p,
+                                                   over, nvalid);
   }
   if (OUT16 && over) atomicOr(status + b, DFC_ST_ENCODE);  // write_depth_png raises (kitti_io.py:60-61)
   if (p.vcount) {
@@ -287,7 +467,7 @@ __device__ __forceinline__ void tile_process(const float* __restrict__ sIn, floa
 // computed, so the latency-bound staging overlaps the ALU-bound median / blur
 // (configs 2 / 4: +4 %).
 template <int MR, int POST, int PR, bool PARTIAL, bool OUT16>
-__global__ void __launch_bounds__(kThreads) blur_tail_kernel(const float* __restrict__ in, void* __restrict__ out_v,
+__global__ void __launch_bounds__(kThreads, DFC_TAIL_MINB) blur_tail_kernel(const float* __restrict__ in, void* __restrict__ out_v,
                                                              int H, int W, uint32_t* __restrict__ status,
                                                              const __grid_constant__ TailParams p, int tx, int ty,
                                                              int64_t ntiles) {
@@ -306,10 +486,10 @@ __global__ void __launch_bounds__(kThreads) blur_tail_kernel(const float* __rest
     asm volatile("cp.async.commit_group;\n" ::: "memory");
     asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // tile t's copies (this thread's)
     __syncthreads();                                          // ... and everyone's
-    const int64_t b = t / ((int64_t)tx * ty);
-    const int r = (int)(t - b * tx * ty), byi = r / tx, bxi = r - byi * tx;
-    tile_process<MR, POST, PR, PARTIAL, OUT16>(cur ? sIn1 : sIn0, sM, out_v, H, W, status, p, b, bxi * G::TX,
-                                               byi * G::TY);
+    const unsigned per = (unsigned)(tx * ty), tu = (unsigned)t;
+    const unsigned b = tu / per, r = tu - b * per, byi = r / (unsigned)tx, bxi = r - byi * (unsigned)tx;
+    tile_process<MR, POST, PR, PARTIAL, OUT16>(cur ? sIn1 : sIn0, sM, out_v, H, W, status, p, (int64_t)b, (int)bxi * G::TX,
+                                               (int)byi * G::TY);
     __syncthreads();  // this tile's input buffer and sM are reused
     cur ^= 1;
   }
@@ -317,7 +497,7 @@ __global__ void __launch_bounds__(kThreads) blur_tail_kernel(const float* __rest
 
 // Without the median: one tile per CTA (plain loads; many resident CTAs hide them).
 template <int MR, int POST, int PR, bool PARTIAL, bool OUT16>
-__global__ void __launch_bounds__(kThreads) blur_tail_tile_kernel(const float* __restrict__ in,
+__global__ void __launch_bounds__(kThreads, DFC_TAIL_MINB) blur_tail_tile_kernel(const float* __restrict__ in,
                                                                   void* __restrict__ out_v, int H, int W,
                                                                   uint32_t* __restrict__ status,
                                                                   const __grid_constant__ TailParams p) {
@@ -340,8 +520,7 @@ cudaError_t launch_t(const float* in, void* out, int64_t B, int H, int W, bool p
                      const TailParams& p, cudaStream_t s) {
   using G = TileGeo<MR, PR>;
   const int tx = (W + G::TX - 1) / G::TX, ty = (H + G::TY - 1) / G::TY;
-  const int64_t ntiles = (int64_t)tx * ty * B;
-  if constexpr (!G::kDB) {
+  if constexpr (!(G::kDB || (POST == kPostBilateral && PR == 2))) {
     // grid.z holds at most 65535 frames: chunk the batch
     const int64_t HW = (int64_t)H * W;
     for (int64_t f0 = 0; f0 < B; f0 += 65535) {
@@ -373,10 +552,20 @@ cudaError_t launch_t(const float* in, void* out, int64_t B, int H, int W, bool p
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kThreads, G::kSmem);
   if (e != cudaSuccess) return e;
-  const int64_t grid = std::min<int64_t>(ntiles, (int64_t)std::max(per, 1) * sms);
-  note_launch();
-  k<<<(unsigned)grid, kThreads, G::kSmem, s>>>(in, out, H, W, status, p, tx, ty, ntiles);
-  return cudaGetLastError();
+  // the kernel indexes tiles in 32 bits: chunk the batch below 2^31 tiles per launch
+  const int64_t HW = (int64_t)H * W, fmax = std::max<int64_t>(1, ((int64_t)1 << 31) / ((int64_t)tx * ty) - 1);
+  for (int64_t f0 = 0; f0 < B; f0 += fmax) {
+    const int64_t C = std::min<int64_t>(fmax, B - f0), nt = (int64_t)tx * ty * C;
+    TailParams pc = p;
+    if (pc.vcount) pc.vcount += 2 * f0;
+    const int64_t grid = std::min<int64_t>(nt, (int64_t)std::max(per, 1) * sms);
+    note_launch();
+    k<<<(unsigned)grid, kThreads, G::kSmem, s>>>(in + f0 * HW, static_cast<char*>(out) + f0 * HW * (out16 ? 2 : 4), H,
+                                                 W, status ? status + f0 : nullptr, pc, tx, ty, nt);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 }  // namespace
@@ -423,6 +612,8 @@ cudaError_t launch_blur_tail(const float* in, void* out, int64_t B, int H, int W
         p.ks[(dy + pr) * k + dx + pr] =
             (float)(l2e * -(double)(dy * dy + dx * dx) / (2.0 * c.bilateral_sigma_space * c.bilateral_sigma_space));
     p.kv = (float)(l2e * -1.0 / (2.0 * c.bilateral_sigma_value * c.bilateral_sigma_value));
+    p.bsc = (float)std::sqrt(l2e / (2.0 * c.bilateral_sigma_value * c.bilateral_sigma_value));
+    p.bisc = (float)(1.0 / std::sqrt(l2e / (2.0 * c.bilateral_sigma_value * c.bilateral_sigma_value)));
   }
   const int mr = med ? c.median_size / 2 : 0;
   const int post = gauss ? kPostGauss : (bil ? kPostBilateral : kPostNone);

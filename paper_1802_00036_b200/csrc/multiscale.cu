@@ -134,7 +134,8 @@ constexpr int kTmNc = 0, kTmM1 = 24, kTmM2 = 32, kTmM3 = 40, kTmF1 = 48, kTmF2 =
 struct MsState {
   F4 fd, nx[kB];
   unsigned um;
-  unsigned nv;  // valid inputs (> 0.1) of the owned columns: RunStats.input_density (pipeline.py:138-141)
+  float2 cnt[2];  // valid inputs (> 0.1) per column pair (RunStats.input_density, pipeline.py:138-141);
+                  // out-of-frame columns load 0, so only the halo lanes 0 / 31 are left out at the end
   uint32_t tm;  // this thread's TMEM lane, column 0
 };
 
@@ -153,18 +154,27 @@ __device__ __forceinline__ void ms_block(MsState& S, const float* __restrict__ s
       set_row(S.nx[j], 0.f);
   }
   F4 nv[kB], mv[kB], fv[kB];
+  // validity and bin membership as 1.0f / 0.0f (one FSET each, ALU pipe); the
+  // selects and the valid-input count (RunStats.input_density, pipeline.py:138-141)
+  // run on the FMA pipe in column pairs: x * 1 and x * 0 are exact, and the
+  // medium bin inv - near - far is exactly inv or +0 (en < ef: one of near / far is 0)
 #pragma unroll
   for (int j = 0; j < kB; ++j)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const float v = cur[j].v[c];
-      S.um = max(S.um, __float_as_uint(v));
-      S.nv += (own >> c & 1u) && v > kValid;  // rows outside the frame are 0
-      const float inv = v > kValid ? p.md - v : 0.0f;  // depth_core.invert
-      const bool near = v <= p.edge_near, far = v > p.edge_far;
-      nv[j].v[c] = near ? inv : 0.0f;
-      fv[j].v[c] = far ? inv : 0.0f;
-      mv[j].v[c] = (near || far) ? 0.0f : inv;
+    for (int h = 0; h < 2; ++h) {
+      const float2 v = make_float2(cur[j].v[2 * h], cur[j].v[2 * h + 1]);
+      S.um = max(max(S.um, __float_as_uint(v.x)), __float_as_uint(v.y));
+      const float2 q = make_float2(v.x > kValid ? 1.f : 0.f, v.y > kValid ? 1.f : 0.f);
+      const float2 qn = make_float2(v.x <= p.edge_near ? 1.f : 0.f, v.y <= p.edge_near ? 1.f : 0.f);
+      const float2 qf = make_float2(v.x > p.edge_far ? 1.f : 0.f, v.y > p.edge_far ? 1.f : 0.f);
+      S.cnt[h] = __fadd2_rn(S.cnt[h], q);  // rows / columns outside the frame are 0
+      // depth_core.invert: (md - v) * valid
+      const float2 inv = __fmul2_rn(__ffma2_rn(v, make_float2(-1.f, -1.f), make_float2(p.md, p.md)), q);
+      const float2 n2 = __fmul2_rn(inv, qn), f2 = __fmul2_rn(inv, qf);
+      const float2 m2 = __fadd2_rn(__fadd2_rn(inv, make_float2(-n2.x, -n2.y)), make_float2(-f2.x, -f2.y));
+      nv[j].v[2 * h] = n2.x, nv[j].v[2 * h + 1] = n2.y;
+      fv[j].v[2 * h] = f2.x, fv[j].v[2 * h + 1] = f2.y;
+      mv[j].v[2 * h] = m2.x, mv[j].v[2 * h + 1] = m2.y;
     }
   // near: FULL7 box (rows t0-3+j)
   F4 nb[kB];
@@ -259,7 +269,7 @@ __device__ __forceinline__ void ms_warp(const float* __restrict__ in, float* __r
   }
   set_row(S.fd, 0.f);
   S.um = 0;
-  S.nv = 0;
+  S.cnt[0] = S.cnt[1] = make_float2(0.f, 0.f);
 #pragma unroll
   for (int j = 0; j < kB; ++j) {
     if (j < H)
@@ -272,7 +282,9 @@ __device__ __forceinline__ void ms_warp(const float* __restrict__ in, float* __r
   else
     ms_rows<VEC, false>(S, src, dst, H, W, x0, oob, own, p);
   const unsigned um = __reduce_max_sync(kFull, S.um);
-  const unsigned nv = __reduce_add_sync(kFull, S.nv);
+  // per-lane counts <= 4 H < 2^24: exact in float
+  const unsigned mine = (unsigned)(S.cnt[0].x + S.cnt[0].y + S.cnt[1].x + S.cnt[1].y);
+  const unsigned nv = __reduce_add_sync(kFull, lane >= 1 && lane <= 30 ? mine : 0u);
   if (lane == 0) atomicMax(umax + b, um);
   if (lane == 0 && nv) atomicAdd(vcount + 2 * b, nv);
 }

@@ -75,6 +75,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU-baseline sample length")
     p.add_argument("--force-staged", action="store_true", help="time the staged (unfused) path instead")
+    p.add_argument("--density", type=float, default=None,
+                   help="override the config's valid-pixel fraction (e.g. 0.0005: sparse frames that need more "
+                        "than one large-fill iteration, the batched device-gated fallback)")
     return p.parse_args()
 
 
@@ -260,7 +263,7 @@ def config_block(B, args):
     from paper_1802_00036_b200 import synth
 
     sp = synth.CONFIG_SPECS[CONFIG_ID]
-    dens = (f"{sp.density[0]:.0%}" if sp.density[0] == sp.density[1]
+    dens = (f"{sp.density[0]:.2%}" if sp.density[0] == sp.density[1]
             else f"U({sp.density[0]:.0%},{sp.density[1]:.0%})")
     batch = (f"a {args.total_frames}-frame batch split over {args.gpus} GPU(s) ({B} per GPU)" if args.total_frames
              else f"{B} synthetic frames per GPU")
@@ -508,6 +511,13 @@ def main():
     global CONFIG_ID
     args = parse()
     CONFIG_ID = args.config
+    if args.density is not None:
+        import dataclasses
+
+        from paper_1802_00036_b200 import synth
+
+        synth.CONFIG_SPECS[CONFIG_ID] = dataclasses.replace(synth.CONFIG_SPECS[CONFIG_ID],
+                                                            density=(args.density, args.density))
     if args.frames is None and args.total_frames is None:
         if CONFIGS[CONFIG_ID][5] == "strong":
             args.total_frames = CONFIGS[CONFIG_ID][3]

@@ -205,7 +205,7 @@ __device__ __forceinline__ void finish_pair(float2 r, float2 c, void* __restrict
 // the exponent is one FFMA2: ks - d'^2 with d' = sc d (prescaled differences
 // round differently from d: ~1e-6 m at most in the output, the bar is 1e-4).
 // fp32 centre-relative: out = c + sum w d / (1 + sum w).
-template <bool PARTIAL, bool OUT16, int MW>
+template <bool PARTIAL, bool OUT16, int MW, bool CST>
 __device__ __forceinline__ void bilateral5_sym(const float* __restrict__ sM, void* __restrict__ out_v, int H, int W,
                                                const TailParams& p, int64_t b, int x0, int y0, bool& over,
                                                unsigned& nvalid) {
@@ -243,8 +243,8 @@ __device__ __forceinline__ void bilateral5_sym(const float* __restrict__ sM, voi
   for (int k = 0; k < 3; ++k) Qa[k] = Qd[k] = make_float2(0.f, 0.f);
 #pragma unroll
   for (int r = 0; r < 3; ++r) load_row(ra + r, V[r], C[r]);
-#pragma unroll
-  for (int i = 0; i < kBand + 2; ++i) {
+  float2 last_r = make_float2(0.f, 0.f);  // the band's first output pair (replicated by the constant path)
+  auto step = [&](const int i) {
     const int s = ra + i;  // sM row (output row s - 2)
     if (i > 0) {
 #pragma unroll
@@ -314,6 +314,7 @@ __device__ __forceinline__ void bilateral5_sym(const float* __restrict__ sM, voi
       const float2 q = __fmul2_rn(make_float2(rcp_approx(den.x), rcp_approx(den.y)), make_float2(p.bisc, p.bisc));
       const float2 c = C[0];
       const float2 r = __ffma2_rn(acc, q, c);
+      last_r = r;
       const int oy = s - 2;
       if (lane != 0 && lane != 31 && oy < rb && y0 + oy < H && gx < W) {
         if (!OUT16 && Weven && gx + 1 < W) {
@@ -332,6 +333,39 @@ __device__ __forceinline__ void bilateral5_sym(const float* __restrict__ sM, voi
     Qa[0] = Qa[1], Qd[0] = Qd[1];
     Qa[1] = Qa[2], Qd[1] = Qd[2];
     Qa[2] = Qd[2] = make_float2(0.f, 0.f);
+  };
+  // A band whose input rows (sM rows ra .. ra + kBand + 3) are vertically
+  // constant in every column -- the rows above every column's first valid row,
+  // which extend_to_top made equal (morphology.py:81-96), or all-empty rows --
+  // has equal output rows: sweep to the first one and store it kBand times.
+  // (CST: without the median; after it, the check's registers cost the
+  // median network more than the shortcut saves, config 2 measured.)
+  bool cst = CST;
+  if (CST) {
+    const float* r0 = sM + ra * MW;
+    const float2 a0 = *reinterpret_cast<const float2*>(r0 + cA), m0 = *reinterpret_cast<const float2*>(r0 + X0),
+                 e0 = *reinterpret_cast<const float2*>(r0 + cC);
+#pragma unroll
+    for (int r = 1; r < kBand + 4; ++r) {
+      const float* rr = r0 + r * MW;
+      const float2 a1 = *reinterpret_cast<const float2*>(rr + cA), m1 = *reinterpret_cast<const float2*>(rr + X0),
+                   e1 = *reinterpret_cast<const float2*>(rr + cC);
+      cst &= __float_as_uint(a1.x) == __float_as_uint(a0.x) && __float_as_uint(a1.y) == __float_as_uint(a0.y) &&
+             __float_as_uint(m1.x) == __float_as_uint(m0.x) && __float_as_uint(m1.y) == __float_as_uint(m0.y) &&
+             __float_as_uint(e1.x) == __float_as_uint(e0.x) && __float_as_uint(e1.y) == __float_as_uint(e0.y);
+    }
+  }
+  if (CST && __all_sync(kFullMask, cst)) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) step(i);
+    const float2 c = C[0];  // = the centre pair of every row
+    for (int oy = ra + 1; oy < rb && y0 + oy < H; ++oy) {
+      if (lane != 0 && lane != 31 && gx < W)
+        finish_pair<PARTIAL, OUT16, true>(last_r, c, out_v, obase + (int64_t)oy * W, gx, W, p, over, nvalid);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < kBand + 2; ++i) step(i);
   }
 }
 
@@ -349,7 +383,7 @@ __device__ __forceinline__ void tile_process(const float* __restrict__ sIn, floa
   if constexpr (MR == 0 && POST == kPostBilateral && PR == 2) {
     // no median: the staged tile (frame-clamped positions = replicate border)
     // is the blur input as it is
-    bilateral5_sym<PARTIAL, OUT16, IWS>(sIn, out_v, H, W, p, b, x0, y0, over, nvalid);
+    bilateral5_sym<PARTIAL, OUT16, IWS, true>(sIn, out_v, H, W, p, b, x0, y0, over, nvalid);
     if (OUT16 && over) atomicOr(status + b, DFC_ST_ENCODE);
     if (p.vcount) {
       nvalid = __reduce_add_sync(0xffffffffu, nvalid);
@@ -403,7 +437,7 @@ __device__ __forceinline__ void tile_process(const float* __restrict__ sIn, floa
   // stage-7b: Gaussian / bilateral, re-impose, invert back -- two horizontally
   // adjacent outputs per thread in packed fp32x2 (FADD2 / FMUL2 / FFMA2)
   if constexpr (POST == kPostBilateral && PR == 2) {
-    bilateral5_sym<PARTIAL, OUT16, MW>(sM, out_v, H, W, p, b, x0, y0, over, nvalid);
+    bilateral5_sym<PARTIAL, OUT16, MW, false>(sM, out_v, H, W, p, b, x0, y0, over, nvalid);
   } else
   for (int i = threadIdx.x; i < kTX * kTY / 2; i += kThreads) {
     const int oy = i / (kTX / 2), ox = 2 * (i - oy * (kTX / 2));

@@ -680,6 +680,7 @@ struct State {
                        // (nearly) always, so the count is H x owned columns unless omin <= 0.1, when
                        // finalize_kernel recounts the frame
   bool had_empty, still_empty;
+  int zrun;            // PARTIAL: consecutive producer blocks with an all-zero inverted input
   uint32_t mbW, mbL, mbR;  // shared addresses of this warp's / the neighbours' P[4], C[4] mbarriers
   bool hasL, hasR;
   int gk;              // block counter across items (mbarrier index and phase)
@@ -750,6 +751,19 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
         stage_lane<VEC>(S.stg + j * 512, q, p.in, !EDGE || t0 + kB + j < H, S.full, S.incol);
       cp_async_commit();
     }
+    // PARTIAL: once the inverted input has been all zero for 6 blocks (24 rows,
+    // more than the stages' 2 x 9-row reach), every stage value the block
+    // produces or carries in TMEM is 0, so the stages are skipped (the rows
+    // above the first LIDAR scanline: about a third of a KITTI-like frame)
+    bool zskip = false;
+    if constexpr (!FULL) {
+      float mx = 0.f;
+#pragma unroll
+      for (int j = 0; j < kB; ++j) mx = fmx3(mx, fmx3(a[j].v[0], a[j].v[1], a[j].v[2]), a[j].v[3]);
+      S.zrun = __all_sync(kFull, mx == 0.f) ? S.zrun + 1 : 0;  // (NaN == 0 is false)
+      zskip = S.zrun > 5;
+    }
+    if (!zskip) {
     // --- stage 2: cross3 o cross3 = 5x5 diamond (rows t0-2+j); PRE: the staged rows ---
     F4 d2[kB];
     if constexpr (PRE) {
@@ -861,6 +875,10 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
           if (t > S.T0[c]) f[j].v[c] = S.top[c];
         }
       }
+    }
+    } else {
+#pragma unroll
+      for (int j = 0; j < kB; ++j) set_row(f[j], 0.f);
     }
   } else {
 #pragma unroll
@@ -1225,6 +1243,7 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
     S.omin = kFMax;
     S.had_empty = S.still_empty = false;
     S.skip = S.fast = S.enc_over = false;
+    S.zrun = 0;
     S.mbW = mb0 + warp * 64;
     S.mbL = mb0 + (warp - 1) * 64;
     S.mbR = mb0 + (warp + 1) * 64;

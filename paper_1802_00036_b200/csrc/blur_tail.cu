@@ -59,6 +59,12 @@ struct TailParams {
     b = hi_;                       \
   } while (0)
 
+// exact median of 5: med3(c, max(min(a, b), min(d, e)), min(max(a, b), max(d, e)))
+__device__ __forceinline__ float med5(float a, float b, float c, float d, float e) {
+  const float f = fmaxf(fminf(a, b), fminf(d, e)), g = fminf(fmaxf(a, b), fmaxf(d, e));
+  return fmaxf(fminf(c, f), fminf(fmaxf(c, f), g));
+}
+
 __device__ __forceinline__ float rcp_approx(float x) {
   float y;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -398,7 +404,33 @@ __device__ __forceinline__ void tile_process(const float* __restrict__ sIn, floa
     const int bx = threadIdx.x % (MW / kMedBlockW), by = threadIdx.x / (MW / kMedBlockW);
     const int mx = bx * kMedBlockW, my = by * kMedBlockH;
     float med[kMedBlockH][kMedBlockW];
-    median5_block(sIn + my * IWS + mx, IWS, med);
+    // The warp's blocks cover median rows 8w .. 8w + 7 of the region; when their
+    // input window (rows 8w .. 8w + 11, all 68 columns) is vertically constant
+    // in every column -- the rows above every column's first valid row, which
+    // extend_to_top made equal (morphology.py:81-96), or empty rows -- each
+    // 5x5 median is the median of its 5 column values (each counted 5 times):
+    // 9 min/max per output instead of ~60.  Each lane checks two columns.
+    bool cst = true;
+    {
+      const float* t = sIn + (threadIdx.x >> 5) * (4 * kMedBlockH) * IWS;
+      const int l = threadIdx.x & 31, ca = 2 * l, cb = 2 * l + 1, cc = min(64 + l, 67);
+      const unsigned b0 = __float_as_uint(t[ca]), b1 = __float_as_uint(t[cb]), b2 = __float_as_uint(t[cc]);
+#pragma unroll
+      for (int r = 1; r < 4 * kMedBlockH + 4; ++r)
+        cst &= __float_as_uint(t[r * IWS + ca]) == b0 && __float_as_uint(t[r * IWS + cb]) == b1 &&
+               __float_as_uint(t[r * IWS + cc]) == b2;
+    }
+    if (__all_sync(0xffffffffu, cst)) {
+      const float* t = sIn + my * IWS + mx;
+#pragma unroll
+      for (int c = 0; c < kMedBlockW; ++c) {
+        const float m = med5(t[c], t[c + 1], t[c + 2], t[c + 3], t[c + 4]);
+#pragma unroll
+        for (int j = 0; j < kMedBlockH; ++j) med[j][c] = m;
+      }
+    } else {
+      median5_block(sIn + my * IWS + mx, IWS, med);
+    }
 #pragma unroll
     for (int j = 0; j < kMedBlockH; ++j) {
 #pragma unroll

@@ -545,6 +545,51 @@ __device__ __noinline__ void lf_vquad(const float* __restrict__ ring, int ringw,
                                       int lane, int c0, bool consecutive, float* __restrict__ V) {
   // vertical 31-maxima of rows c0 .. c0+3 (windows [c_j - 15, c_j + 15]); the
   // rows [c0-12, c0+15] are common to all four
+  constexpr int kNC = (kVC + 31) / 32;  // columns per lane: sc = lane + 32 i
+  if (consecutive && c0 - kLF >= 0 && c0 + kB - 1 + kLF < H) {
+    // every window row lies inside the frame: walk the 34 ring rows once (the
+    // slot sequence is the same for all columns), each row feeding the lane's
+    // five columns -- no per-load clamp or modulo
+    float core[kNC], u15[kNC], u14[kNC], u13[kNC], d16[kNC], d17[kNC], d18[kNC];
+    bool ok[kNC];
+#pragma unroll
+    for (int i = 0; i < kNC; ++i) {
+      const int sc = lane + 32 * i, col = L - kVOff + sc;
+      ok[i] = sc < kVC && col >= p0 && col < p1;
+    }
+    const float* cb = ring + (L - kVOff + lane - p0);
+    int slot = (c0 - kLF + PLAG) % kRing;  // c0 >= 15 here
+#pragma unroll
+    for (int k = 0; k < 2 * kLF + kB; ++k) {
+      const float* rp = cb + slot * ringw;
+#pragma unroll
+      for (int i = 0; i < kNC; ++i) {
+        float v = 0.f;
+        if (ok[i]) v = rp[32 * i];
+        if (k == 0) u15[i] = v;
+        else if (k == 1) u14[i] = v;
+        else if (k == 2) u13[i] = v;
+        else if (k == 3) core[i] = v;
+        else if (k < 2 * kLF + 1) core[i] = fmx(core[i], v);
+        else if (k == 2 * kLF + 1) d16[i] = v;
+        else if (k == 2 * kLF + 2) d17[i] = v;
+        else d18[i] = v;
+      }
+      slot = slot + 1 == kRing ? 0 : slot + 1;
+    }
+#pragma unroll
+    for (int i = 0; i < kNC; ++i) {
+      const int sc = lane + 32 * i;
+      if (sc < kVC) {
+        V[0 * kVC + sc] = fmx(core[i], fmx3(u15[i], u14[i], u13[i]));
+        V[1 * kVC + sc] = fmx3(core[i], fmx(u14[i], u13[i]), d16[i]);
+        V[2 * kVC + sc] = fmx3(core[i], u13[i], fmx(d16[i], d17[i]));
+        V[3 * kVC + sc] = fmx(core[i], fmx3(d16[i], d17[i], d18[i]));
+      }
+    }
+    __syncwarp();
+    return;
+  }
 #pragma unroll 1
   for (int sc = lane; sc < kVC; sc += 32) {
     const int col = L - kVOff + sc;
@@ -555,24 +600,13 @@ __device__ __noinline__ void lf_vquad(const float* __restrict__ ring, int ringw,
         const int rr = r < 0 ? 0 : (r >= H ? H - 1 : r);
         return rc[((rr + PLAG) % kRing) * ringw];
       };
-      if (consecutive) {
-        float core = ld(c0 - 12);
-#pragma unroll 9
-        for (int r = c0 - 11; r <= c0 + 15; ++r) core = fmx(core, ld(r));
-        const float u15 = ld(c0 - 15), u14 = ld(c0 - 14), u13 = ld(c0 - 13);
-        const float d16 = ld(c0 + 16), d17 = ld(c0 + 17), d18 = ld(c0 + 18);
-        o[0] = fmx(core, fmx3(u15, u14, u13));
-        o[1] = fmx3(core, fmx(u14, u13), d16);
-        o[2] = fmx3(core, u13, fmx(d16, d17));
-        o[3] = fmx(core, fmx3(d16, d17, d18));
-      } else {  // frame ends: each row centre clamped separately
+      // near the frame ends: each row centre and window clamped separately
 #pragma unroll
-        for (int j = 0; j < kB; ++j) {
-          const int cj = min(max(c0 + j, 0), H - 1);
-          float m = ld(cj - kLF);
-          for (int r = cj - kLF + 1; r <= cj + kLF; ++r) m = fmx(m, ld(r));
-          o[j] = m;
-        }
+      for (int j = 0; j < kB; ++j) {
+        const int cj = min(max(c0 + j, 0), H - 1);
+        float m = ld(cj - kLF);
+        for (int r = cj - kLF + 1; r <= cj + kLF; ++r) m = fmx(m, ld(r));
+        o[j] = m;
       }
     }
 #pragma unroll

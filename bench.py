@@ -358,6 +358,9 @@ def run_ours(args):
     ms = MultiscaleConfig() if multi else None
     cfg = to_dfc_config(config, multiscale=ms, force_staged=args.force_staged)
     cfg.flags |= _lib.F_NO_FINISH
+    sparse = args.density is not None and args.density < 0.025  # what complete_batch's auto hint would pick
+    if sparse:
+        cfg.flags |= _lib.F_SPARSE
     L = _lib.load()
     need = int(L.dfc_workspace_bytes(ctypes.byref(cfg), B, H, W))
     ws = torch.empty(need, dtype=torch.uint8, device=dev)
@@ -500,7 +503,7 @@ def run_ours(args):
                 "data": "synthetic (seeded, SURVEY 8(d))",
                 "config": config_block(B, args), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "e2e_raw16": e2e_raw16,
-                "clocks": clk, "gpu_launches": launches, "fallback_frames_per_step": n_fallback,
+                "clocks": clk, "gpu_launches": launches, "fallback_frames_per_step": n_fallback, "sparse_hint": sparse,
                 "gpu": torch.cuda.get_device_name(dev)}
         print(json.dumps(line), flush=True)
     if world > 1:

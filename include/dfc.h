@@ -86,6 +86,9 @@ extern "C" {
 #define DFC_F_FORCE_STAGED 0x1u /* never use the fused kernel */
 #define DFC_F_EXACT_BLUR 0x2u   /* fp64 blurs in the reference's operation order */
 #define DFC_F_NO_FINISH 0x4u    /* dfc_fill_batch does not synchronize; call dfc_fill_finish */
+#define DFC_F_SPARSE 0x8u       /* performance hint, results unchanged: frames with many empty pixels after the
+                                   small fill (about <= 2 % valid inputs) -- the fused kernel's register-dense
+                                   large fill (without it, dense frames run ~2 % faster) */
 
 /* PipelineConfig (pipeline.py:50-89) + inversion offset + multiscale bins. */
 typedef struct dfc_config {

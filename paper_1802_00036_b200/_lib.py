@@ -30,6 +30,7 @@ ST_FALLBACK = 0x100
 F_FORCE_STAGED = 0x1
 F_EXACT_BLUR = 0x2
 F_NO_FINISH = 0x4
+F_SPARSE = 0x8  # performance hint: register-dense large fill (frames with many empties); results unchanged
 
 SHAPE_CODES = {"full": 0, "circle": 1, "cross": 2, "diamond": 3}
 BLUR_CODES = {"none": 0, "bilateral": 1, "median": 2, "median_bilateral": 3, "gaussian": 4,

@@ -191,9 +191,22 @@ def _device() -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
 
 
+# Input density below which the previous batch on a device selects the fused
+# kernel's register-dense large fill for the next one (DFC_F_SPARSE; dense
+# frames run ~2 % faster without it, 1 %-density frames 2.4x faster with it).
+SPARSE_DENSITY = 0.025
+_last_sparse: dict[int, bool] = {}
+
+
 def complete_batch(frames, config: PipelineConfig | None = None, multiscale: MultiscaleConfig | None = None,
-                   custom_offsets=None, raise_on_error: bool = True, force_staged: bool = False) -> ops.FillResult:
-    """Complete a [B, H, W] batch (torch CUDA tensor, or host array copied in)."""
+                   custom_offsets=None, raise_on_error: bool = True, force_staged: bool = False,
+                   sparse_hint: bool | None = None) -> ops.FillResult:
+    """Complete a [B, H, W] batch (torch CUDA tensor, or host array copied in).
+
+    ``sparse_hint`` (performance only, results are identical): True / False
+    selects / skips the register-dense large fill for frames with many empty
+    pixels; None (default) follows the input density the previous call
+    measured on this device."""
     config = config or PipelineConfig()
     if isinstance(frames, np.ndarray):
         frames = np.ascontiguousarray(frames, dtype=np.float32)
@@ -205,9 +218,15 @@ def complete_batch(frames, config: PipelineConfig | None = None, multiscale: Mul
     if frames.dim() == 2:
         frames = frames.unsqueeze(0)
     cfg = to_dfc_config(config, multiscale, custom_offsets, force_staged)
+    dev = frames.device.index or 0
+    if sparse_hint if sparse_hint is not None else _last_sparse.get(dev, False):
+        cfg.flags |= _lib.F_SPARSE
     res = ops.fill_batch(frames, cfg)
     if raise_on_error:
         raise_for_status(res.status.cpu().numpy(), _max_depth(config))
+    if res.valid_counts is not None and res.dense.numel():
+        n_in = float(res.valid_counts[:, 0].sum().item())
+        _last_sparse[dev] = n_in / res.dense.numel() < SPARSE_DENSITY
     return res
 
 

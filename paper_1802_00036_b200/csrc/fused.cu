@@ -229,6 +229,7 @@ cudaError_t launch_fused(const void* in_v, void* out_v, int64_t B, int H, int W,
   p.SW = L.SW;
   p.nw = L.nw;
   p.dense = L.dense;
+  p.regdense = (c.flags & DFC_F_SPARSE) ? 1 : 0;
   p.md = c.max_depth;
   {
     // only the in-kernel Gaussian (size 5) uses these taps; every other blur

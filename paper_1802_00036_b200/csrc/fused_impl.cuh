@@ -102,6 +102,7 @@ struct Params {
   void* out;
   int64_t nframes;
   int dense;  // shared-memory scratch for the dense large fill is available
+  int regdense;  // DFC_F_SPARSE: use the register-dense large-fill instantiation
   int32_t* t0g;  // FULL: per-column r0 row (processing order) from r0_kernel, [nframes][W]
   int H, W, strips, SW, nw;
   float md;
@@ -539,6 +540,12 @@ __device__ __forceinline__ float lf_rows(const float* __restrict__ ring, int rin
 // L-11 .. L+140 into V[4][kVC] (34 ring rows per column), then each lane takes
 // the horizontal 31-max of its own empty pixels from V.
 constexpr int kVC = 152, kVOff = 11, kDenseMin = 12;
+constexpr int kRegDenseMin = 6;  // lf_regdense from this many eligible empties per warp block (~6 per-pixel passes)
+// large-fill strategies (fused kernel template parameter DENSE): per-pixel
+// warp passes only; + the shared-scratch dense pass (wide strips, config 4);
+// + the register-dense pass (DFC_F_SPARSE: its code in the loop costs dense
+// frames ~2 %, so it is a separate instantiation)
+constexpr int kLfSparse = 0, kLfSmemDense = 1, kLfRegDense = 2;
 
 template <int PLAG>
 __device__ __noinline__ void lf_vquad(const float* __restrict__ ring, int ringw, int p0, int p1, int H, int L,
@@ -636,6 +643,76 @@ __device__ __forceinline__ F4 lf_hquad(const float* __restrict__ V, int j, int l
              fmx(core, fmx3(d16, d17, d18))}};
 }
 
+// Register-dense large fill (many empty pixels in a warp's block, no shared
+// scratch needed): the vertical 31-row maxima of the block's four rows for the
+// lane's own four columns (one walk over the 34 ring rows, two columns per
+// 8-byte load), then each row's horizontal 31-max from the lanes l-4 .. l+4 by
+// shuffles: lanes l-3 .. l+3 whole (a sliding max over 7 lanes), lane l-4's
+// suffix and lane l+4's prefix maxima for the partial ends.  Exact for the
+// columns whose window lies inside the warp's 128 columns (x in [L+15, L+112]);
+// the caller keeps the others on the per-pixel passes.  Needs every window row
+// inside the frame.  Values are >= 0, out-of-strip columns count as 0.
+template <int PLAG>
+__device__ __forceinline__ void lf_regdense(const float* __restrict__ ring, int ringw, int p0, int p1, int x0,
+                                            int c0, F4 (&w)[kB]) {
+  float vm[kB][4];
+  int slot0 = (c0 - kLF + PLAG) % kRing;  // c0 >= 15 here
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {  // column pairs (0, 1), (2, 3)
+    const int xa = x0 + 2 * h;
+    const bool oka = xa >= p0 && xa < p1, okb = xa + 1 >= p0 && xa + 1 < p1;
+    const float* cb = ring + (xa - p0);
+    float u15[2], u14[2], u13[2], core[2], d16[2], d17[2], d18[2];
+    int slot = slot0;
+#pragma unroll
+    for (int k = 0; k < 2 * kLF + kB; ++k) {
+      float2 q = make_float2(0.f, 0.f);
+      if (oka && okb) q = *reinterpret_cast<const float2*>(cb + slot * ringw);
+      else if (oka) q.x = cb[slot * ringw];
+      else if (okb) q.y = cb[slot * ringw + 1];
+      const float v[2] = {q.x, q.y};
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        if (k == 0) u15[i] = v[i];
+        else if (k == 1) u14[i] = v[i];
+        else if (k == 2) u13[i] = v[i];
+        else if (k == 3) core[i] = v[i];
+        else if (k < 2 * kLF + 1) core[i] = fmx(core[i], v[i]);
+        else if (k == 2 * kLF + 1) d16[i] = v[i];
+        else if (k == 2 * kLF + 2) d17[i] = v[i];
+        else d18[i] = v[i];
+      }
+      slot = slot + 1 == kRing ? 0 : slot + 1;
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      vm[0][2 * h + i] = fmx(core[i], fmx3(u15[i], u14[i], u13[i]));
+      vm[1][2 * h + i] = fmx3(core[i], fmx(u14[i], u13[i]), d16[i]);
+      vm[2][2 * h + i] = fmx3(core[i], u13[i], fmx(d16[i], d17[i]));
+      vm[3][2 * h + i] = fmx(core[i], fmx3(d16[i], d17[i], d18[i]));
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kB; ++j) {
+    const float* g = vm[j];
+    const float M = fmx(fmx3(g[0], g[1], g[2]), g[3]);
+    const float A = fmx(M, __shfl_down_sync(kFull, M, 1));
+    const float Bm = fmx(A, __shfl_down_sync(kFull, A, 2));
+    const float C = fmx(Bm, __shfl_down_sync(kFull, Bm, 3));
+    const float F = __shfl_up_sync(kFull, C, 3);  // max over lanes l-3 .. l+3
+    const float s2 = fmx(g[2], g[3]), s1 = fmx(g[1], s2);
+    const float p1_ = fmx(g[0], g[1]), p2_ = fmx(p1_, g[2]);
+    const float Ls1 = __shfl_up_sync(kFull, s1, 4), Ls2 = __shfl_up_sync(kFull, s2, 4);
+    const float Ls3 = __shfl_up_sync(kFull, g[3], 4);
+    const float Rp0 = __shfl_down_sync(kFull, g[0], 4), Rp1 = __shfl_down_sync(kFull, p1_, 4);
+    const float Rp2 = __shfl_down_sync(kFull, p2_, 4);
+    w[j].v[0] = fmx(F, Ls1);
+    w[j].v[1] = fmx3(F, Ls2, Rp0);
+    w[j].v[2] = fmx3(F, Ls3, Rp1);
+    w[j].v[3] = fmx(F, Rp2);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Tensor memory as a per-thread store for the rows each stage carries from
 // one block to the next (TMEM is otherwise idle here: no MMA).  Each warp owns
@@ -724,7 +801,7 @@ struct State {
   int compR;           // component of column W - 1 in this lane, else -1
 };
 
-template <int VEC, bool FULL, int BLUR, bool PRE, bool DENSE, int IO, bool EDGE>
+template <int VEC, bool FULL, int BLUR, bool PRE, int DENSE, int IO, bool EDGE>
 __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
   using TIn = typename IoT<IO>::In;
   using TOut = typename IoT<IO>::Out;
@@ -1010,7 +1087,29 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
       // neighbours' rows up to tc0 + 18
       if (S.hasL) mb_wait(S.mbL + (g & 3) * 8, (g >> 2) & 1);
       if (S.hasR) mb_wait(S.mbR + (g & 3) * 8, (g >> 2) & 1);
-      if (DENSE && __reduce_add_sync(kFull, __popc(em)) > kDenseMin) {
+      if constexpr (DENSE == kLfRegDense) {
+        // many empties: the register-dense pass for the columns it covers
+        // columns whose 31-wide window lies in the warp's lanes: x in [L + 15, L + 112]
+        const unsigned elc = (S.lane >= 4 && S.lane <= 27) ? 0xFu
+                             : (S.lane == 3 ? 0x8u : (S.lane == 28 ? 0x1u : 0u));
+        const unsigned el = em & (elc * 0x1111u);
+        if (tc0 - kLF >= 0 && tc0 + kB - 1 + kLF < H &&
+            __reduce_add_sync(kFull, __popc(el)) > kRegDenseMin) {
+          F4 wv[kB];
+          lf_regdense<LG::P>(S.ring, S.ringw, S.p0, S.p1, S.x0, tc0, wv);
+#pragma unroll
+          for (int j = 0; j < kB; ++j)
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              if (el >> (4 * j + c) & 1u) {
+                v6[j].v[c] = wv[j].v[c];
+                S.still_empty |= !(wv[j].v[c] > kValid);
+              }
+          em &= ~el;
+          lanes = __ballot_sync(kFull, em != 0);
+        }
+      }
+      if (DENSE == kLfSmemDense && __reduce_add_sync(kFull, __popc(em)) > kDenseMin) {
         float* V = S.ring + kRing * S.ringw + p.nw * (kB * 128) + (threadIdx.x >> 5) * (kB * kVC);
         lf_vquad<LG::P>(S.ring, S.ringw, S.p0, S.p1, H, S.L, S.lane, tc0, !EDGE || (tc0 >= 0 && tc0 + kB - 1 < H),
                         V);
@@ -1197,7 +1296,7 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
 // ---------------------------------------------------------------------------
 // the fused kernel
 // ---------------------------------------------------------------------------
-template <int VEC, bool FULL, int BLUR, bool PRE, bool DENSE, int IO>
+template <int VEC, bool FULL, int BLUR, bool PRE, int DENSE, int IO>
 __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constant__ Params p) {
   using TIn = typename IoT<IO>::In;
   using TOut = typename IoT<IO>::Out;
@@ -1265,6 +1364,7 @@ __global__ void __launch_bounds__(kNW * 32, 1) fused_kernel(const __grid_constan
     }
     S.incol = incol;
     S.needm = needm;
+
     S.full = incol == 0xFu;
     S.woob = __any_sync(kFull, S.oob != 0);
     S.edgeL = S.x0 == 0;                                           // lane holding column 0
@@ -1470,7 +1570,7 @@ __global__ void __launch_bounds__(128, 4) r0_kernel(const __grid_constant__ Para
   }
 }
 
-template <int VEC, bool FULL, int BLUR, bool PRE, bool DENSE = false, int IO = 0>
+template <int VEC, bool FULL, int BLUR, bool PRE, int DENSE = kLfSparse, int IO = 0>
 cudaError_t launch_t(const Params& p, size_t smem, int grid, cudaStream_t s) {
   if constexpr (FULL) {
     const int64_t warps = p.nframes * p.strips * p.nw;
@@ -1500,7 +1600,15 @@ cudaError_t dispatch_blur(int blur, bool pre, const Params& p, size_t smem, int 
 // DENSE (shared-memory scratch for the dense large fill): FULL mode, wide strips, W % 4 == 0
 template <int BLUR>
 cudaError_t dispatch_dense(bool pre, const Params& p, size_t smem, int grid, cudaStream_t s) {
-  return pre ? launch_t<4, true, BLUR, true, true>(p, smem, grid, s) : launch_t<4, true, BLUR, false, true>(p, smem, grid, s);
+  return pre ? launch_t<4, true, BLUR, true, kLfSmemDense>(p, smem, grid, s)
+             : launch_t<4, true, BLUR, false, kLfSmemDense>(p, smem, grid, s);
+}
+
+// DFC_F_SPARSE (FULL mode, narrow strips): the register-dense large fill
+template <int BLUR>
+cudaError_t dispatch_regdense(bool pre, const Params& p, size_t smem, int grid, cudaStream_t s) {
+  return pre ? launch_t<4, true, BLUR, true, kLfRegDense>(p, smem, grid, s)
+             : launch_t<4, true, BLUR, false, kLfRegDense>(p, smem, grid, s);
 }
 
 }  // namespace

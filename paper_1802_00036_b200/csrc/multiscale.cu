@@ -100,6 +100,7 @@ constexpr int kMsWarps = 4;
 
 struct MsFastParams {
   float md, edge_near, edge_far;
+  int64_t nframes;
 };
 
 __device__ __forceinline__ F4 cross3(const F4& up, const F4& mid, const F4& dn) {
@@ -242,8 +243,7 @@ __device__ __forceinline__ void ms_rows(MsState& S, const float* src, float* dst
 template <int VEC>
 __device__ __forceinline__ void ms_warp(const float* __restrict__ in, float* __restrict__ out, int H, int W,
                                         unsigned* __restrict__ umax, unsigned* __restrict__ vcount,
-                                        const MsFastParams& p, int S0, int lane, uint32_t tm) {
-  const int64_t b = blockIdx.y;
+                                        const MsFastParams& p, int64_t b, int S0, int lane, uint32_t tm) {
   const float* src = in + b * (int64_t)H * W;
   float* dst = out + b * (int64_t)H * W;
   const int x0 = S0 - 4 + 4 * lane;
@@ -303,8 +303,15 @@ __global__ void __launch_bounds__(kMsWarps * 32, 4) ms_fast_kernel(const float* 
   __syncthreads();
   tm_fence_after();
   const uint32_t tmbase = s_tm;
-  const int S0 = (blockIdx.x * kMsWarps + warp) * kMsOwn;
-  if (S0 < W) ms_warp<VEC>(in, out, H, W, umax, vcount, p, S0, lane, tmbase + ((uint32_t)(warp * 32) << 16));
+  // warps are numbered over (frame, 120-column slice) pairs, so a CTA may span
+  // two frames and no warp of a CTA idles at the frame's right edge (with one
+  // CTA per 480 columns, half the warps of the last CTA of a 1216-wide frame had
+  // no columns and held their slot)
+  const int nwf = (W + kMsOwn - 1) / kMsOwn;  // warps per frame
+  const int64_t gw = (int64_t)blockIdx.x * kMsWarps + warp;
+  if (gw < p.nframes * nwf)
+    ms_warp<VEC>(in, out, H, W, umax, vcount, p, gw / nwf, (int)(gw % nwf) * kMsOwn, lane,
+                 tmbase + ((uint32_t)(warp * 32) << 16));
   tm_wait_st();
   tm_fence_before();
   __syncthreads();
@@ -330,8 +337,10 @@ cudaError_t launch_multiscale_stage2(const float* in, float* out, int64_t B, int
                                      const int32_t* const offs[3], const int n[3], unsigned* umax, unsigned* vcount,
                                      cudaStream_t s) {
   if (multiscale_fast_kernels(c)) {
-    MsFastParams q{c.max_depth, c.bin_edge_near, c.bin_edge_far};
-    const dim3 grid((unsigned)((W + kMsOwn * kMsWarps - 1) / (kMsOwn * kMsWarps)), (unsigned)B);
+    MsFastParams q{c.max_depth, c.bin_edge_near, c.bin_edge_far, 0};
+    q.nframes = B;
+    const int64_t nw = B * ((W + kMsOwn - 1) / kMsOwn);
+    const unsigned grid = (unsigned)((nw + kMsWarps - 1) / kMsWarps);
     note_launch();
     if (W % 4 == 0)
       ms_fast_kernel<4><<<grid, kMsWarps * 32, 0, s>>>(in, out, H, W, umax, vcount, q);

@@ -355,6 +355,27 @@ def test_fused_random_sparse_frames(P):
             assert int(res.iterations[i]) == info["large_fill_iterations"]
 
 
+@pytest.mark.parametrize("density", [0.01, 0.002])
+def test_low_density_scanline_frames(P, density):
+    """BASELINE config-1 frames at 1 % / 0.2 % density (~12 % / ~60 % of the
+    pixels still empty after the small fill): the register-dense large fill
+    (warp blocks with many empties), the per-pixel passes around it and, at
+    0.2 %, the batched multi-iteration fallback, against the oracle."""
+    import dataclasses
+
+    spec = dataclasses.replace(synth.CONFIG_SPECS[1], density=(density, density))
+    frames = np.stack([synth.make_frame(spec, [1, 9000 + i]) for i in range(2)])
+    for blur in ("none", "gaussian"):
+        kw = {"blur_mode": blur, "fill_mode": "full"}
+        refs = [O.complete_with_stats(frames[i], _ocfg(kw)) for i in range(frames.shape[0])]
+        for hint in (True, False):  # DFC_F_SPARSE: the register-dense large fill or the per-pixel passes
+            res = P.complete_batch(frames, _pcfg(P, kw), sparse_hint=hint)
+            got = res.dense.cpu().numpy()
+            for i, (ref, info) in enumerate(refs):
+                _cmp(got[i], ref, blur)
+                assert int(res.iterations[i]) == info["large_fill_iterations"]
+
+
 MS_DEFAULT = ((15.0, 30.0), (O.KernelShape.FULL, 7), (O.KernelShape.DIAMOND, 7), (O.KernelShape.DIAMOND, 5))
 
 

@@ -101,6 +101,7 @@ constexpr int kMsWarps = 4;
 struct MsFastParams {
   float md, edge_near, edge_far;
   int64_t nframes;
+  int nseg, seg_rows;  // row segments per column slice, rows per segment (a multiple of 4)
 };
 
 __device__ __forceinline__ F4 cross3(const F4& up, const F4& mid, const F4& dn) {
@@ -142,9 +143,13 @@ struct MsState {
 
 // one 4-row block: input rows t0..t0+3 in, output rows t0-3..t0 out.  EDGE:
 // rows may lie outside the frame; WOOB: the warp has out-of-frame columns.
+// EDGE blocks also carry the row segment [ya, yb) the warp stores (rows outside
+// it belong to the neighbouring segments, or are warm-up) and whether this
+// block's input rows count towards the valid-input sum.
 template <int VEC, bool EDGE, bool WOOB>
 __device__ __forceinline__ void ms_block(MsState& S, const float* __restrict__ src, float* __restrict__ dst, int t0,
-                                         int H, int W, int x0, unsigned oob, unsigned own, const MsFastParams& p) {
+                                         int H, int W, int x0, unsigned oob, unsigned own, const MsFastParams& p,
+                                         int ya = 0, int yb = 0, bool cnt_on = true) {
   F4 cur[kB];
 #pragma unroll
   for (int j = 0; j < kB; ++j) {
@@ -168,7 +173,7 @@ __device__ __forceinline__ void ms_block(MsState& S, const float* __restrict__ s
       const float2 q = make_float2(v.x > kValid ? 1.f : 0.f, v.y > kValid ? 1.f : 0.f);
       const float2 qn = make_float2(v.x <= p.edge_near ? 1.f : 0.f, v.y <= p.edge_near ? 1.f : 0.f);
       const float2 qf = make_float2(v.x > p.edge_far ? 1.f : 0.f, v.y > p.edge_far ? 1.f : 0.f);
-      S.cnt[h] = __fadd2_rn(S.cnt[h], q);  // rows / columns outside the frame are 0
+      if (!EDGE || cnt_on) S.cnt[h] = __fadd2_rn(S.cnt[h], q);  // rows / columns outside the frame are 0
       // depth_core.invert: (md - v) * valid
       const float2 inv = __fmul2_rn(__ffma2_rn(v, make_float2(-1.f, -1.f), make_float2(p.md, p.md)), q);
       const float2 n2 = __fmul2_rn(inv, qn), f2 = __fmul2_rn(inv, qf);
@@ -221,7 +226,7 @@ __device__ __forceinline__ void ms_block(MsState& S, const float* __restrict__ s
 #pragma unroll
   for (int j = 0; j < kB; ++j) {
     const int y = t0 - 3 + j;
-    if (EDGE && (y < 0 || y >= H)) continue;
+    if (EDGE && (y < ya || y >= yb)) continue;
     F4 o;
 #pragma unroll
     for (int c = 0; c < 4; ++c) o.v[c] = fmx3(nb[j].v[c], a3[j].v[c], fr[j].v[c]);
@@ -229,21 +234,31 @@ __device__ __forceinline__ void ms_block(MsState& S, const float* __restrict__ s
   }
 }
 
+// Output rows [ya, yb) of the warp's columns (ya a multiple of 4; yb one too,
+// or H).  A segment that starts inside the frame streams one warm-up block
+// first: with zero carries, outputs from 3 rows below the first streamed row
+// are exact (each output row depends on input rows y - 3 .. y + 3 only).
 template <int VEC, bool WOOB>
 __device__ __forceinline__ void ms_rows(MsState& S, const float* src, float* dst, int H, int W, int x0, unsigned oob,
-                                        unsigned own, const MsFastParams& p) {
-  // the lean body needs every row it touches inside the frame: stages and
+                                        unsigned own, const MsFastParams& p, int ya, int yb) {
+  // the lean body needs every row it touches inside the frame -- stages and
   // outputs down to t0 - 3 (t0 >= 4), the prefetch up to t0 + 7 (t0 + 8 <= H)
-  int t0 = 0;
-  for (; t0 < 4 && t0 < H + 3; t0 += kB) ms_block<VEC, true, WOOB>(S, src, dst, t0, H, W, x0, oob, own, p);
-  for (; t0 + 2 * kB <= H; t0 += kB) ms_block<VEC, false, WOOB>(S, src, dst, t0, H, W, x0, oob, own, p);
-  for (; t0 < H + 3; t0 += kB) ms_block<VEC, true, WOOB>(S, src, dst, t0, H, W, x0, oob, own, p);
+  // -- and its four output rows t0 - 3 .. t0 inside the segment
+  int t0 = ya >= kB ? ya - kB : 0;
+  const int tend = yb >= H ? H + 3 : yb + 1;  // the block at t0 = yb holds the segment's last rows
+  const int lean0 = max(ya + kB, 4);
+  for (; t0 < lean0 && t0 < tend; t0 += kB)
+    ms_block<VEC, true, WOOB>(S, src, dst, t0, H, W, x0, oob, own, p, ya, yb, t0 >= ya && t0 < yb);
+  for (; t0 + kB <= yb && t0 + 2 * kB <= H; t0 += kB) ms_block<VEC, false, WOOB>(S, src, dst, t0, H, W, x0, oob, own, p);
+  for (; t0 < tend; t0 += kB)
+    ms_block<VEC, true, WOOB>(S, src, dst, t0, H, W, x0, oob, own, p, ya, yb, t0 >= ya && t0 < yb);
 }
 
 template <int VEC>
 __device__ __forceinline__ void ms_warp(const float* __restrict__ in, float* __restrict__ out, int H, int W,
                                         unsigned* __restrict__ umax, unsigned* __restrict__ vcount,
-                                        const MsFastParams& p, int64_t b, int S0, int lane, uint32_t tm) {
+                                        const MsFastParams& p, int64_t b, int S0, int ya, int yb, int lane,
+                                        uint32_t tm) {
   const float* src = in + b * (int64_t)H * W;
   float* dst = out + b * (int64_t)H * W;
   const int x0 = S0 - 4 + 4 * lane;
@@ -270,17 +285,18 @@ __device__ __forceinline__ void ms_warp(const float* __restrict__ in, float* __r
   set_row(S.fd, 0.f);
   S.um = 0;
   S.cnt[0] = S.cnt[1] = make_float2(0.f, 0.f);
+  const int ts = ya >= kB ? ya - kB : 0;  // first streamed row (ms_rows)
 #pragma unroll
   for (int j = 0; j < kB; ++j) {
-    if (j < H)
-      S.nx[j] = load4<VEC, true>(src + (int64_t)j * W, x0, W);
+    if (ts + j < H)
+      S.nx[j] = load4<VEC, true>(src + (int64_t)(ts + j) * W, x0, W);
     else
       set_row(S.nx[j], 0.f);
   }
   if (__any_sync(kFull, oob != 0))
-    ms_rows<VEC, true>(S, src, dst, H, W, x0, oob, own, p);
+    ms_rows<VEC, true>(S, src, dst, H, W, x0, oob, own, p, ya, yb);
   else
-    ms_rows<VEC, false>(S, src, dst, H, W, x0, oob, own, p);
+    ms_rows<VEC, false>(S, src, dst, H, W, x0, oob, own, p, ya, yb);
   const unsigned um = __reduce_max_sync(kFull, S.um);
   // per-lane counts <= 4 H < 2^24: exact in float
   const unsigned mine = (unsigned)(S.cnt[0].x + S.cnt[0].y + S.cnt[1].x + S.cnt[1].y);
@@ -307,11 +323,19 @@ __global__ void __launch_bounds__(kMsWarps * 32, 4) ms_fast_kernel(const float* 
   // two frames and no warp of a CTA idles at the frame's right edge (with one
   // CTA per 480 columns, half the warps of the last CTA of a 1216-wide frame had
   // no columns and held their slot)
-  const int nwf = (W + kMsOwn - 1) / kMsOwn;  // warps per frame
+  // ... and over row segments: a round of 296 frames x 11 slices is 1.4 waves
+  // of the 16 warps per SM, so whole-column items left the second wave 37 %
+  // full (config 4: 9 %); with p.nseg segments per column the last wave is a
+  // fraction of an item.  Items of a frame's segment are adjacent.
+  const int nwf = (W + kMsOwn - 1) / kMsOwn;  // warps per (frame, segment)
   const int64_t gw = (int64_t)blockIdx.x * kMsWarps + warp;
-  if (gw < p.nframes * nwf)
-    ms_warp<VEC>(in, out, H, W, umax, vcount, p, gw / nwf, (int)(gw % nwf) * kMsOwn, lane,
+  if (gw < p.nframes * p.nseg * nwf) {
+    const int64_t fs = gw / nwf;
+    const int seg = (int)(fs % p.nseg);
+    const int ya = seg * p.seg_rows, yb = min(H, ya + p.seg_rows);
+    ms_warp<VEC>(in, out, H, W, umax, vcount, p, fs / p.nseg, (int)(gw % nwf) * kMsOwn, ya, yb, lane,
                  tmbase + ((uint32_t)(warp * 32) << 16));
+  }
   tm_wait_st();
   tm_fence_before();
   __syncthreads();
@@ -337,9 +361,28 @@ cudaError_t launch_multiscale_stage2(const float* in, float* out, int64_t B, int
                                      const int32_t* const offs[3], const int n[3], unsigned* umax, unsigned* vcount,
                                      cudaStream_t s) {
   if (multiscale_fast_kernels(c)) {
-    MsFastParams q{c.max_depth, c.bin_edge_near, c.bin_edge_far, 0};
+    MsFastParams q{c.max_depth, c.bin_edge_near, c.bin_edge_far, 0, 1, 0};
     q.nframes = B;
-    const int64_t nw = B * ((W + kMsOwn - 1) / kMsOwn);
+    // Row segments per column slice (each adds one 4-row warm-up block and the
+    // per-item set-up).  Whole columns are best while they fill the GPU evenly
+    // (measured: config 2's 1.4 waves lose 2.5 % to 4 segments -- a thin second
+    // wave runs faster, the kernel is issue-bound per SM); segments pay when the
+    // last wave is nearly empty (config 4: 1.09 waves, +4.5 % with 4 segments)
+    // or the batch does not fill the SMs at all (single frames, small batches).
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t slots = (int64_t)sms * 4 * kMsWarps, items = B * ((W + kMsOwn - 1) / kMsOwn);
+    int nseg = 1;
+    if (items < slots)  // measured on 1216x352: 20 % off the whole call for batches of 1-16 frames, 13 % at 32
+      nseg = (int)std::min<int64_t>(std::max<int64_t>(4, slots / (4 * items)), 16);
+    else if (items > slots && items % slots != 0 && items % slots < slots / 4)
+      nseg = 4;
+    if (getenv("DFC_MS_NSEG")) nseg = atoi(getenv("DFC_MS_NSEG"));  // A/B runs
+    q.nseg = std::max(1, std::min(nseg, H / 32));
+    q.seg_rows = (((H + kB - 1) / kB + q.nseg - 1) / q.nseg) * kB;
+    q.nseg = (H + q.seg_rows - 1) / q.seg_rows;
+    const int64_t nw = B * q.nseg * ((W + kMsOwn - 1) / kMsOwn);
     const unsigned grid = (unsigned)((nw + kMsWarps - 1) / kMsWarps);
     note_launch();
     if (W % 4 == 0)

@@ -393,6 +393,30 @@ def test_multiscale_geometries_vs_oracle(P, h, w, blur, fill):
         assert int(res.iterations[i]) == info["large_fill_iterations"]
 
 
+@pytest.mark.parametrize("h,w", [(352, 1216), (100, 250), (67, 130), (1024, 512)])
+def test_multiscale_row_segments_bit_identical(P, h, w, monkeypatch):
+    """The stage-2 streaming kernel cuts column slices into row segments (one warm-up block each) when whole
+    columns do not fill the SMs evenly; every segment count gives the whole-column result bit for bit, the
+    same valid-input counts, and matches the composed oracle."""
+    frames = synth.make_batch(2, 900, 2) if (h, w) == (352, 1216) else _geom_frames(h, w, 2, h + w)
+    kw = {"blur_mode": "none", "fill_mode": "full"}
+    outs = {}
+    for nseg in ("1", "2", "3", "4", "16"):
+        monkeypatch.setenv("DFC_MS_NSEG", nseg)
+        res = P.complete_batch(frames, _pcfg(P, kw), multiscale=P.MultiscaleConfig())
+        outs[nseg] = (res.dense.cpu().numpy(), res.valid_counts.cpu().numpy()[:, 0])
+    monkeypatch.delenv("DFC_MS_NSEG")
+    res = P.complete_batch(frames, _pcfg(P, kw), multiscale=P.MultiscaleConfig())
+    outs["auto"] = (res.dense.cpu().numpy(), res.valid_counts.cpu().numpy()[:, 0])
+    for k, (d, n) in outs.items():
+        assert d.tobytes() == outs["1"][0].tobytes(), k
+        assert np.array_equal(n, outs["1"][1]), k
+    for i in range(frames.shape[0]):
+        ref = O.complete(frames[i], O.OracleConfig(**{**_ocfg(kw).__dict__, "multiscale": MS_DEFAULT}))
+        _cmp(outs["auto"][0][i], ref, "none")
+        assert int(outs["auto"][1][i]) == int(np.count_nonzero(frames[i] > 0.1))
+
+
 @pytest.mark.parametrize("kernels", [((O.KernelShape.CROSS, 5), (O.KernelShape.CIRCLE, 7), (O.KernelShape.FULL, 3)),
                                      ((O.KernelShape.DIAMOND, 3), (O.KernelShape.FULL, 5), (O.KernelShape.CIRCLE, 5))])
 def test_multiscale_other_kernels_vs_oracle(P, kernels):

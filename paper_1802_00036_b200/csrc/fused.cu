@@ -185,25 +185,34 @@ bool raw_mode(const dfc_config& c) {
 
 size_t raw_offset(int64_t B) { return ((16 + (size_t)B * 4) + 255) & ~(size_t)255; }
 
-// frames per fused round when intermediate maps go through the workspace:
-// two CTA waves on a 148-SM B200
-int64_t round_frames(const dfc_config& c, int64_t B, int W) {
+// Frames per round when intermediate maps go through the workspace (the
+// stage-6 map of the raw mode, the stage-2 map of multiscale): every kernel of
+// a round (stage 2 -> fused -> blur tail) ramps up and drains once per round, so
+// rounds are as long as an 8 GiB budget of maps allows, between 2 and 32 CTA
+// waves of a 148-SM B200 (measured on 1024-frame batches against 2-wave
+// rounds: config 2 +8 %, config 4 +2 %, config 0 +1.3 %; the maps do not fit L2
+// either way).  DFC_RAW_CHUNK sets the items per round for A/B runs.
+int64_t round_frames(const dfc_config& c, int64_t B, int H, int W) {
   if (!raw_mode(c) && !c.multiscale) return B;
-  const int64_t ch = (kRawChunk + layout(W).strips - 1) / layout(W).strips;
+  const int64_t strips = layout(W).strips;
+  const int64_t forced = getenv("DFC_RAW_CHUNK") ? atoll(getenv("DFC_RAW_CHUNK")) : 0;  // read per call: tests set it
+  const int64_t lo = (kRawChunk + strips - 1) / strips, hi = (16 * kRawChunk + strips - 1) / strips;
+  const int64_t fit = (int64_t)(((size_t)8 << 30) / ((size_t)2 * H * W * 4));
+  const int64_t ch = forced ? (forced + strips - 1) / strips : std::max(lo, std::min(hi, fit));
   return B < ch ? B : ch;
 }
 
-size_t t0_bytes(const dfc_config& c, int64_t B, int W) {
-  return c.fill_mode == DFC_FILL_FULL ? (((size_t)round_frames(c, B, W) * W * 4 + 255) & ~(size_t)255) : 0;
+size_t t0_bytes(const dfc_config& c, int64_t B, int H, int W) {
+  return c.fill_mode == DFC_FILL_FULL ? (((size_t)round_frames(c, B, H, W) * W * 4 + 255) & ~(size_t)255) : 0;
 }
 
 size_t fused_workspace_bytes(const dfc_config& c, int64_t B, int H, int W) {
   // [0] u64 frames needing the staged path, [8] u32 work counter, [16..) u32 umax[B],
   // then one round of stage-6 maps (raw mode), of stage-2 maps (multiscale) and
   // of per-column r0 rows (FULL)
-  const size_t map = (size_t)round_frames(c, B, W) * H * W * 4;
+  const size_t map = (size_t)round_frames(c, B, H, W) * H * W * 4;
   const size_t a = (map + 255) & ~(size_t)255;
-  return raw_offset(B) + (raw_mode(c) ? a : 0) + (c.multiscale ? a : 0) + t0_bytes(c, B, W) + 256;
+  return raw_offset(B) + (raw_mode(c) ? a : 0) + (c.multiscale ? a : 0) + t0_bytes(c, B, H, W) + 256;
 }
 
 bool fused_supports_raw16(const dfc_config& c, int H, int W) {
@@ -265,7 +274,7 @@ cudaError_t launch_fused(const void* in_v, void* out_v, int64_t B, int H, int W,
   const int blur = raw ? kBlurRaw : c.blur_mode;
   const int64_t HW = (int64_t)H * W;
   const bool pre = c.multiscale != 0;
-  const int64_t chunk = round_frames(c, B, W);
+  const int64_t chunk = round_frames(c, B, H, W);
   const size_t map = (((size_t)chunk * HW * 4) + 255) & ~(size_t)255;
   float* tmp = raw ? reinterpret_cast<float*>(w8 + raw_offset(B)) : nullptr;
   float* s2 = pre ? reinterpret_cast<float*>(w8 + raw_offset(B) + (raw ? map : 0)) : nullptr;

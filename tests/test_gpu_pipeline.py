@@ -393,6 +393,27 @@ def test_multiscale_geometries_vs_oracle(P, h, w, blur, fill):
         assert int(res.iterations[i]) == info["large_fill_iterations"]
 
 
+@pytest.mark.parametrize("multi", [False, True])
+def test_rounds_bit_identical(P, multi, monkeypatch):
+    """Raw-mode / multiscale batches run in rounds whose intermediate maps live in the workspace; the round
+    length (an 8 GiB budget by default) must not change a bit: 3 and 2 rounds against one."""
+    frames = synth.make_batch(2, 700, 20)
+    cfg = _pcfg(P, {"blur_mode": "median_bilateral", "fill_mode": "full"})
+    ms = P.MultiscaleConfig() if multi else None
+    outs = []
+    for chunk in ("8", "12", None):
+        if chunk:
+            monkeypatch.setenv("DFC_RAW_CHUNK", chunk)
+        else:
+            monkeypatch.delenv("DFC_RAW_CHUNK")
+        res = P.complete_batch(frames, cfg, multiscale=ms)
+        outs.append((res.dense.cpu().numpy(), res.valid_counts.cpu().numpy(), res.iterations.cpu().numpy()))
+        assert not (res.status.cpu().numpy() & 0xFF).any()
+    for d, n, it in outs[:-1]:
+        assert d.tobytes() == outs[-1][0].tobytes()
+        assert np.array_equal(n, outs[-1][1]) and np.array_equal(it, outs[-1][2])
+
+
 @pytest.mark.parametrize("h,w", [(352, 1216), (100, 250), (67, 130), (1024, 512)])
 def test_multiscale_row_segments_bit_identical(P, h, w, monkeypatch):
     """The stage-2 streaming kernel cuts column slices into row segments (one warm-up block each) when whole

@@ -114,7 +114,7 @@ cudaError_t launch_blur_tail(const float* in, void* out, int64_t B, int H, int W
 bool multiscale_stage2_supported(const dfc_config& c);
 cudaError_t launch_multiscale_stage2(const float* in, float* out, int64_t B, int H, int W, const dfc_config& c,
                                      const int32_t* const offs[3], const int n[3], unsigned* umax, unsigned* vcount,
-                                     cudaStream_t s);
+                                     unsigned* work, cudaStream_t s);  // work: a zeroed device counter (item queue)
 
 // ---- fused pipeline (fused.cu) -------------------------------------------
 struct FusedPlan;

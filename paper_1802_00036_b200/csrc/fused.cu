@@ -295,8 +295,10 @@ cudaError_t launch_fused(const void* in_v, void* out_v, int64_t B, int H, int W,
   }
   for (int64_t f0 = 0; f0 < B; f0 += chunk) {
     const int64_t C = B - f0 < chunk ? B - f0 : chunk;
+    // the stage-2 kernel's item queue is the word after the fused kernel's (zeroed with it above)
+    if (pre && f0 > 0 && (e = cudaMemsetAsync(p.work + 1, 0, 4, s)) != cudaSuccess) return e;
     if (pre && (e = launch_multiscale_stage2(in + f0 * HW, s2, C, H, W, c, op, on, umax0 + f0, vcount + 2 * f0,
-                                             s)) != cudaSuccess)
+                                             p.work + 1, s)) != cudaSuccess)
       return e;
     char* out_c = static_cast<char*>(out_v) + f0 * HW * osz;
     p.in = pre ? (const void*)s2 : (const void*)(static_cast<const char*>(in_v) + f0 * HW * isz);

@@ -271,6 +271,7 @@ __device__ __forceinline__ void ms_warp(const float* __restrict__ in, float* __r
   }
   MsState S;
   S.tm = tm;
+  tm_wait_st();  // the previous item's carry stores (persistent warps)
   {
     F4 z[6];
 #pragma unroll
@@ -310,6 +311,7 @@ __global__ void __launch_bounds__(kMsWarps * 32, 4) ms_fast_kernel(const float* 
                                                                    float* __restrict__ out, int H, int W,
                                                                    unsigned* __restrict__ umax,
                                                                    unsigned* __restrict__ vcount,
+                                                                   unsigned* __restrict__ work,
                                                                    const __grid_constant__ MsFastParams p) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   static_assert(kMsWarps == 4, "one warp per TMEM lane quarter");
@@ -327,10 +329,18 @@ __global__ void __launch_bounds__(kMsWarps * 32, 4) ms_fast_kernel(const float* 
   // of the 16 warps per SM, so whole-column items left the second wave 37 %
   // full (config 4: 9 %); with p.nseg segments per column the last wave is a
   // fraction of an item.  Items of a frame's segment are adjacent.
-  const int nwf = (W + kMsOwn - 1) / kMsOwn;  // warps per (frame, segment)
-  const int64_t gw = (int64_t)blockIdx.x * kMsWarps + warp;
-  if (gw < p.nframes * p.nseg * nwf) {
-    const int64_t fs = gw / nwf;
+  const int nwf = (W + kMsOwn - 1) / kMsOwn;  // items per (frame, segment)
+  // Warps are persistent and take items from a queue: a warp that finishes
+  // (interior slices are ~20 % cheaper than the frame-edge ones) starts its
+  // next item at once instead of holding its slot until the CTA's slowest
+  // warp reaches the closing barrier.
+  const unsigned total = (unsigned)(p.nframes * p.nseg * nwf);
+  for (;;) {
+    unsigned gw = 0;
+    if (lane == 0) gw = atomicAdd(work, 1u);
+    gw = __shfl_sync(kFull, gw, 0);
+    if (gw >= total) break;
+    const unsigned fs = gw / nwf;
     const int seg = (int)(fs % p.nseg);
     const int ya = seg * p.seg_rows, yb = min(H, ya + p.seg_rows);
     ms_warp<VEC>(in, out, H, W, umax, vcount, p, fs / p.nseg, (int)(gw % nwf) * kMsOwn, ya, yb, lane,
@@ -359,7 +369,7 @@ bool multiscale_stage2_supported(const dfc_config& c) {
 
 cudaError_t launch_multiscale_stage2(const float* in, float* out, int64_t B, int H, int W, const dfc_config& c,
                                      const int32_t* const offs[3], const int n[3], unsigned* umax, unsigned* vcount,
-                                     cudaStream_t s) {
+                                     unsigned* work, cudaStream_t s) {
   if (multiscale_fast_kernels(c)) {
     MsFastParams q{c.max_depth, c.bin_edge_near, c.bin_edge_far, 0, 1, 0};
     q.nframes = B;
@@ -383,14 +393,14 @@ cudaError_t launch_multiscale_stage2(const float* in, float* out, int64_t B, int
     q.seg_rows = (((H + kB - 1) / kB + q.nseg - 1) / q.nseg) * kB;
     q.nseg = (H + q.seg_rows - 1) / q.seg_rows;
     const int64_t nw = B * q.nseg * ((W + kMsOwn - 1) / kMsOwn);
-    const unsigned grid = (unsigned)((nw + kMsWarps - 1) / kMsWarps);
+    const unsigned grid = (unsigned)std::min<int64_t>((nw + kMsWarps - 1) / kMsWarps, (int64_t)sms * 4);
     note_launch();
     if (W % 4 == 0)
-      ms_fast_kernel<4><<<grid, kMsWarps * 32, 0, s>>>(in, out, H, W, umax, vcount, q);
+      ms_fast_kernel<4><<<grid, kMsWarps * 32, 0, s>>>(in, out, H, W, umax, vcount, work, q);
     else if (W % 2 == 0)
-      ms_fast_kernel<2><<<grid, kMsWarps * 32, 0, s>>>(in, out, H, W, umax, vcount, q);
+      ms_fast_kernel<2><<<grid, kMsWarps * 32, 0, s>>>(in, out, H, W, umax, vcount, work, q);
     else
-      ms_fast_kernel<1><<<grid, kMsWarps * 32, 0, s>>>(in, out, H, W, umax, vcount, q);
+      ms_fast_kernel<1><<<grid, kMsWarps * 32, 0, s>>>(in, out, H, W, umax, vcount, work, q);
     return cudaGetLastError();
   }
   BinParams p{};

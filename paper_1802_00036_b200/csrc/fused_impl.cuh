@@ -932,8 +932,18 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
       for (int j = 0; j < kB; ++j) m5[j] = hwin2<OpMax>(ext_row<2>(vv[j]));
 #pragma unroll
       for (int j = 0; j < kB; ++j) {
-        if (EDGE && (t0 - L2 - 2 + j < 0 || t0 - L2 - 2 + j >= H)) set_row(m5[j], kFMax);
-        if (S.woob) fix_oob(m5[j], S.oob, kFMax);
+        if constexpr (VEC == 4) {
+          // W % 4 == 0: a lane lies wholly inside or outside the frame, so the fix is four selects on one
+          // lane predicate instead of a mask test per column (the edge warps pace their CTA: +1 %)
+          if (S.woob) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) m5[j].v[c] = S.oob ? kFMax : m5[j].v[c];
+          }
+          if (EDGE && (t0 - L2 - 2 + j < 0 || t0 - L2 - 2 + j >= H)) set_row(m5[j], kFMax);
+        } else {
+          if (EDGE && (t0 - L2 - 2 + j < 0 || t0 - L2 - 2 + j >= H)) set_row(m5[j], kFMax);
+          if (S.woob) fix_oob(m5[j], S.oob, kFMax);
+        }
       }
     }
     // --- close: min5 (rows t0-L2-4+j) ---
@@ -950,7 +960,14 @@ __device__ __forceinline__ void iterate(const Params& p, State& S, int k) {
 #pragma unroll
       for (int j = 0; j < kB; ++j) {
         if (EDGE && (t0 - L2 - 4 + j < 0 || t0 - L2 - 4 + j >= H)) set_row(cl[j], 0.f);
-        if (S.woob) fix_oob(cl[j], S.oob, 0.f);
+        if constexpr (VEC == 4) {
+          if (S.woob) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) cl[j].v[c] = S.oob ? 0.f : cl[j].v[c];
+          }
+        } else if (S.woob) {
+          fix_oob(cl[j], S.oob, 0.f);
+        }
       }
     }
     // --- small fill: masked max7 (rows t0-L2-7+j = tp+j) ---
